@@ -1,0 +1,132 @@
+/*
+ * fmmbem_b200 — C ABI of the B200 (sm_100a) FMM-BEM hot path.
+ *
+ * The reference (arXiv:1506.05957 package, /root/reference/pkg/src/fmmbem) is
+ * pure Python; its plug-in point for this path is a Python duck type, not an
+ * FFI: solver.gmres(apply_fn, ...) calls apply_fn(x, p) (solver.py:69,99) and
+ * solver.solve(operator, ...) passes operator.apply (solver.py:142).  Each
+ * entry point below replaces one method of that surface; the ctypes binding
+ * that mirrors the reference classes is paper_1506_05957_b200/_native.py and
+ * INTEGRATION.md shows the binding a maintainer of the reference would add.
+ *
+ * Conventions: every function returns 0 on success, FMMBEM_EINVAL for invalid
+ * arguments (the reference raises ValueError) and FMMBEM_ECUDA for device
+ * failures; fmmbem_last_error() returns the thread's last message.  Arrays are
+ * C-contiguous float64 / int64 in the reference's own shapes and orders.
+ * "host" buffers are ordinary memory; *_device variants take device pointers.
+ * Handles are not re-entrant (one stream per operator, like the reference's
+ * sequential solver loop).
+ */
+#ifndef FMMBEM_B200_H
+#define FMMBEM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMMBEM_OK 0
+#define FMMBEM_EINVAL 1
+#define FMMBEM_ECUDA 2
+#define FMMBEM_EINTERNAL 3
+
+typedef struct fmmbem_plan fmmbem_plan;
+typedef struct fmmbem_op fmmbem_op;
+
+/* Formulation enum values (bemop.py:33-40). */
+#define FMMBEM_LAPLACE_FIRST 0
+#define FMMBEM_LAPLACE_SECOND 1
+#define FMMBEM_STOKES 2
+
+const char* fmmbem_last_error(void);
+int fmmbem_version(void);
+/* number of visible CUDA devices (0 on a CPU-only host; never an error) */
+int fmmbem_device_count(int* count);
+/* measured sm_100a DFMA throughput (TFLOP/s) of a dependent-chain microkernel */
+int fmmbem_fp64_peak(int device, double* tflops);
+
+/* ---------------------------------------------------------------- FmmPlan
+ * Replaces fmm.FmmPlan.__init__ (fmm.py:131-168): shared bounding cube
+ * (octree.bounding_cube, octree.py:46-54), both octrees (octree.build_tree,
+ * octree.py:57-131) and the dual traversal (fmm.dual_traversal, fmm.py:84-125),
+ * all built on the device.  src_xyz (ns,3), tgt_xyz (nt,3). */
+int fmmbem_plan_create(const double* src_xyz, int64_t ns, const double* tgt_xyz, int64_t nt,
+                       int n_crit, double theta, int max_depth, int device, fmmbem_plan** out);
+int fmmbem_plan_destroy(fmmbem_plan* plan);
+/* sizes[0..9] = src cells, tgt cells, src leaves, tgt leaves, m2l pairs, p2p pairs,
+ *               src levels, tgt levels, p2p interactions, m2l offsets */
+int fmmbem_plan_sizes(const fmmbem_plan* plan, int64_t* sizes);
+/* Octree arrays of one tree (which = 0 source, 1 target), mirrors octree.Octree
+ * (octree.py:6-43).  Cells are numbered level by level, Morton order inside a
+ * level (the reference numbers depth-first); compare by content. Any output
+ * pointer may be NULL. center (ncell,3). */
+int fmmbem_plan_tree(const fmmbem_plan* plan, int which, int64_t* perm, double* center,
+                     double* half_width, int32_t* level, int32_t* parent, int64_t* body_start,
+                     int64_t* body_count, uint8_t* is_leaf);
+/* Interaction lists (which = 0 M2L, 1 P2P) as (n,2) int32 (source cell, target cell),
+ * like FmmPlan.m2l_pairs / p2p_pairs (fmm.py:141-143). */
+int fmmbem_plan_pairs(const fmmbem_plan* plan, int which, int32_t* pairs);
+/* FmmPlan.far_field (parts=1, fmm.py:203-233) and/or near_field (parts=2,
+ * fmm.py:356-419) of the 1/r kernel with C in {1,4,7} channels of charges (C,ns)
+ * and/or dipoles (C,ns,3).  pot (C,nt) and grad (C,nt,3, may be NULL) are
+ * OVERWRITTEN with the requested parts' sum (no 1/4pi). Host buffers. */
+int fmmbem_plan_evaluate(fmmbem_plan* plan, const double* charges, const double* dipoles, int C,
+                         int p, int want_gradient, int parts, double* pot, double* grad);
+
+/* ---------------------------------------------------------------- BemOperator
+ * Replaces bemop.BemOperator.__init__ (bemop.py:50-82): geometry comes from the
+ * host (quadrature.quadrature_points / panel_geometry, quadrature.py:86-121, so
+ * it is bit-identical to the reference), the plan, the near-pair search
+ * (bemop.py:95-101) and both correction matrices (bemop.py:127-184, including
+ * the polar singular integrals quadrature.py:175-247) are built on the device.
+ *   panel_vertices (P,3,3), gauss_pts (P,4,3), gauss_wts (P,4) — FAR_RULE;
+ *   fine_pts (P,19,3), fine_wts (P,19) — NEAR_RULE; normals (P,3); areas (P);
+ *   leg_x / leg_w — n_gauss_singular Gauss-Legendre nodes on [-1,1]. */
+int fmmbem_op_create(const double* panel_vertices, int64_t n_panels, const double* gauss_pts,
+                     const double* gauss_wts, const double* fine_pts, const double* fine_wts,
+                     const double* normals, const double* areas, const double* leg_x,
+                     const double* leg_w, int n_gauss_singular, int formulation, double theta,
+                     int n_crit, double mu, double near_factor, int max_depth, int device,
+                     fmmbem_op** out);
+int fmmbem_op_destroy(fmmbem_op* op);
+/* number of unknowns n (BemOperator.shape[0], bemop.py:89-92) */
+int fmmbem_op_size(const fmmbem_op* op, int64_t* n);
+/* borrowed plan handle of the operator (BemOperator.plan) — do not destroy */
+int fmmbem_op_plan(fmmbem_op* op, fmmbem_plan** plan);
+/* BemOperator.apply(x, p) (bemop.py:272-274), host x (n) -> host y (n) */
+int fmmbem_op_apply(fmmbem_op* op, const double* x, double* y, int p);
+/* same with device pointers, stream-ordered on the op's stream; synchronises
+ * before returning.  stream is reserved (pass NULL). */
+int fmmbem_op_apply_device(fmmbem_op* op, const double* x_dev, double* y_dev, int p, void* stream);
+/* BemOperator.dense_apply(x) (bemop.py:276-278) */
+int fmmbem_op_dense_apply(fmmbem_op* op, const double* x, double* y);
+/* BemOperator.assemble_rhs(data, p, dense) (bemop.py:290-310); data (P) or (P,3) */
+int fmmbem_op_assemble_rhs(fmmbem_op* op, const double* data, int p, int dense, double* b);
+/* Correction CSR (which = 0 C_sys, 1 C_rhs), rows = target panels, columns ascending,
+ * block = 1 (Laplace) or 9 (Stokes 3x3 row-major).  Call with NULL arrays to get
+ * nnz_pairs and block; indptr (P+1), indices (nnz), data (nnz*block). */
+int fmmbem_op_correction(const fmmbem_op* op, int which, int64_t* nnz_pairs, int32_t* block,
+                         int64_t* indptr, int64_t* indices, double* data);
+/* solver.solve / solver.gmres with the relaxation schedule (solver.py:20-143) on
+ * the device.  Host b (n) -> host x (n); residuals / orders (max_iter) are filled
+ * for the n_iter iterations done. */
+int fmmbem_op_gmres(fmmbem_op* op, const double* b, double tol, int p_initial, int p_min,
+                    int relaxed, int max_iter, double* x, double* residuals, int32_t* orders,
+                    int32_t* n_iter, int32_t* converged);
+/* device-pointer GMRES (b_dev, x_dev on the op's device) */
+int fmmbem_op_gmres_device(fmmbem_op* op, const double* b_dev, double tol, int p_initial,
+                           int p_min, int relaxed, int max_iter, double* x_dev,
+                           double* residuals, int32_t* orders, int32_t* n_iter,
+                           int32_t* converged);
+/* instrumentation: enable per-stage CUDA-event timing of every apply (0/1), read
+ * the accumulated milliseconds per stage [p2p, p2m+m2m, m2l, l2l, epilogue, total]
+ * and the number of timed applies, reset them; use_graphs toggles CUDA graphs. */
+int fmmbem_op_set_timing(fmmbem_op* op, int enable, int use_graphs);
+int fmmbem_op_stage_times(fmmbem_op* op, double* ms6, int64_t* calls, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FMMBEM_B200_H */

@@ -1,0 +1,192 @@
+// Shared device/host helpers for the B200 FMM-BEM hot path.
+//
+// Coefficient storage convention (differs from the reference on purpose):
+// the reference keeps all (p+1)^2 complex coefficients per expansion in the
+// flat n^2+n+m layout (harmonics.py:30-35).  Sources and densities are real,
+// so M_n^{-m} = (-1)^m conj(M_n^m) (harmonics.py:56-58) and the same holds for
+// local expansions and for R / I.  Here every expansion stores only m >= 0:
+// index hidx(n, m) = n(n+1)/2 + m, count hcount(p) = (p+1)(p+2)/2, which halves
+// memory traffic and M2L work.  Negative orders are reconstructed on the fly.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace fmmbem {
+
+constexpr int P_MAX = 20;             // largest expansion order served (RHS uses 18)
+constexpr int MAX_DEPTH_LIMIT = 21;   // 3 bits per level in a 64-bit key
+
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgumentError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+#define FMM_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t err__ = (call);                                                          \
+    if (err__ != cudaSuccess)                                                            \
+      throw ::fmmbem::CudaFailure(std::string(#call) + ": " + cudaGetErrorString(err__) + \
+                                  " (" __FILE__ ":" + std::to_string(__LINE__) + ")");   \
+  } while (0)
+
+#define FMM_LAUNCH_CHECK() FMM_CUDA(cudaGetLastError())
+
+#define FMM_REQUIRE(cond, msg)                  \
+  do {                                          \
+    if (!(cond)) throw ::fmmbem::ArgumentError(msg); \
+  } while (0)
+
+__host__ __device__ constexpr int hidx(int n, int m) { return n * (n + 1) / 2 + m; }
+__host__ __device__ constexpr int hcount(int p) { return (p + 1) * (p + 2) / 2; }
+
+// ---------------------------------------------------------------- complex on double2
+__device__ __forceinline__ double2 cmake(double re, double im) { return make_double2(re, im); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// acc + a * b
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+// acc + a * conj(b)
+__device__ __forceinline__ double2 cfma_conj(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.y, b.x, acc.y);
+  acc.y = fma(-a.x, b.y, acc.y);
+  return acc;
+}
+
+// value of a half-stored real-symmetric expansion at (n, m), any sign of m
+__device__ __forceinline__ double2 hget(const double2* c, int n, int m) {
+  if (m >= 0) return c[hidx(n, m)];
+  double2 v = c[hidx(n, -m)];
+  return (m & 1) ? make_double2(-v.x, v.y) : make_double2(v.x, -v.y);
+}
+
+// ------------------------------------------------ solid harmonics (harmonics.py:38-85)
+// Regular R_n^m(r) = rho^n P_n^m e^{im b}/(n+m)!, m >= 0, n <= p, into out[hidx].
+__device__ inline void regular_half(double x, double y, double z, int p, double2* out) {
+  const double rho2 = x * x + y * y + z * z;
+  double2 diag = make_double2(1.0, 0.0);
+  for (int m = 0; m <= p; ++m) {
+    if (m > 0) {
+      // R_m^m = -(x + i y) / (2m) * R_{m-1}^{m-1}
+      const double s = -1.0 / (2.0 * m);
+      diag = cscale(cmul(make_double2(x, y), diag), s);
+    }
+    out[hidx(m, m)] = diag;
+    if (m + 1 <= p) {
+      double2 prev2 = diag;
+      double2 prev1 = cscale(diag, z);
+      out[hidx(m + 1, m)] = prev1;
+      for (int n = m + 2; n <= p; ++n) {
+        const double inv = 1.0 / (double)((n + m) * (n - m));
+        double2 cur;
+        cur.x = ((2 * n - 1) * z * prev1.x - rho2 * prev2.x) * inv;
+        cur.y = ((2 * n - 1) * z * prev1.y - rho2 * prev2.y) * inv;
+        out[hidx(n, m)] = cur;
+        prev2 = prev1;
+        prev1 = cur;
+      }
+    }
+  }
+}
+
+// Irregular I_n^m(r) = (n-m)! P_n^m e^{im b} / rho^(n+1), m >= 0, n <= p.
+__device__ inline void irregular_half(double x, double y, double z, int p, double2* out) {
+  const double rho2 = x * x + y * y + z * z;
+  const double inv_r2 = 1.0 / rho2;
+  double2 diag = make_double2(1.0 / sqrt(rho2), 0.0);
+  for (int m = 0; m <= p; ++m) {
+    if (m > 0) {
+      // I_m^m = -(2m-1)(x + i y)/rho^2 * I_{m-1}^{m-1}
+      const double s = -(2.0 * m - 1.0) * inv_r2;
+      diag = cscale(cmul(make_double2(x, y), diag), s);
+    }
+    out[hidx(m, m)] = diag;
+    if (m + 1 <= p) {
+      double2 prev2 = diag;
+      double2 prev1 = cscale(diag, (2.0 * m + 1.0) * z * inv_r2);
+      out[hidx(m + 1, m)] = prev1;
+      for (int n = m + 2; n <= p; ++n) {
+        const double a = (2 * n - 1) * z;
+        const double b = (double)((n - 1) * (n - 1) - m * m);
+        double2 cur;
+        cur.x = (a * prev1.x - b * prev2.x) * inv_r2;
+        cur.y = (a * prev1.y - b * prev2.y) * inv_r2;
+        out[hidx(n, m)] = cur;
+        prev2 = prev1;
+        prev1 = cur;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- device buffer
+template <typename T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { resize(n); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr_(o.ptr_), n_(o.n_) { o.ptr_ = nullptr; o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); ptr_ = o.ptr_; n_ = o.n_; o.ptr_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  void resize(size_t n) {
+    if (n == n_) return;
+    release();
+    if (n) FMM_CUDA(cudaMalloc(&ptr_, n * sizeof(T)));
+    n_ = n;
+  }
+  void ensure(size_t n) { if (n > n_) resize(n); }
+  void release() {
+    if (ptr_) cudaFree(ptr_);
+    ptr_ = nullptr;
+    n_ = 0;
+  }
+  void zero(cudaStream_t s = 0) { if (n_) FMM_CUDA(cudaMemsetAsync(ptr_, 0, n_ * sizeof(T), s)); }
+  void upload(const T* h, size_t n, cudaStream_t s = 0) {
+    resize(n);
+    if (n) FMM_CUDA(cudaMemcpyAsync(ptr_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s = 0) { upload(v.data(), v.size(), s); }
+  std::vector<T> download(cudaStream_t s = 0) const {
+    std::vector<T> h(n_);
+    if (n_) {
+      FMM_CUDA(cudaMemcpyAsync(h.data(), ptr_, n_ * sizeof(T), cudaMemcpyDeviceToHost, s));
+      FMM_CUDA(cudaStreamSynchronize(s));
+    }
+    return h;
+  }
+  T* get() const { return ptr_; }
+  size_t size() const { return n_; }
+
+ private:
+  T* ptr_ = nullptr;
+  size_t n_ = 0;
+};
+
+inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
+
+}  // namespace fmmbem

@@ -1,0 +1,203 @@
+// Relaxed GMRES with the Krylov basis resident in HBM.
+//
+// Reference: solver.gmres (solver.py:69-134), RelaxationSchedule / schedule_p /
+// relax_eps (solver.py:20-47).  Unrestarted, modified Gram-Schmidt Arnoldi and
+// Givens rotations, residual estimate |g[k+1]| / ||b||, stop when < tol, then
+// y = H^{-1} g and x = sum y_j v_j.  The mat-vec, the MGS dot/axpy sweeps, the
+// norm and the basis update run on the device; the O(k) Givens/Hessenberg
+// scalar work and the order schedule run on the host from one (k+2)-double
+// read-back per iteration, which is also the only host synchronisation.
+// Reductions are two-level with a fixed combination order (bitwise
+// reproducible from run to run).
+#include <cmath>
+
+#include "operator.cuh"
+
+namespace fmmbem {
+namespace {
+
+constexpr int RT = 256;   // threads per reduction block
+constexpr int RB = 296;   // blocks (2 per SM)
+
+__device__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+  __syncthreads();
+  return t;
+}
+
+// finish: the last block to arrive adds the block partials in block order
+__device__ void finish(double part, double* partials, unsigned* counter, double* out, bool do_sqrt) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = part;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) t += ((volatile double*)partials)[b];
+    *out = do_sqrt ? sqrt(t) : t;
+    *counter = 0u;
+  }
+}
+
+// w -= h_prev * v_prev (if v_prev); out = v . w      (solver.py:100-102)
+__global__ void __launch_bounds__(RT) k_mgs(int64_t n, const double* __restrict__ v, double* w,
+                                            const double* __restrict__ vprev, const double* hprev,
+                                            double* partials, unsigned* counter, double* out) {
+  __shared__ double sh[RT / 32];
+  const double h = vprev ? *hprev : 0.0;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double wi = w[i];
+    if (vprev) {
+      wi = wi - h * vprev[i];
+      w[i] = wi;
+    }
+    acc = fma(v[i], wi, acc);
+  }
+  finish(block_sum(acc, sh), partials, counter, out, false);
+}
+
+// w -= h * v; out = ||w||    (solver.py:102-103)
+__global__ void __launch_bounds__(RT) k_norm(int64_t n, double* w, const double* __restrict__ v,
+                                             const double* hv, double* partials, unsigned* counter,
+                                             double* out) {
+  __shared__ double sh[RT / 32];
+  const double h = v ? *hv : 0.0;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double wi = w[i];
+    if (v) {
+      wi = wi - h * v[i];
+      w[i] = wi;
+    }
+    acc = fma(wi, wi, acc);
+  }
+  finish(block_sum(acc, sh), partials, counter, out, true);
+}
+
+// v = w / h (or zeros on breakdown)    (solver.py:104-107)
+__global__ void k_normalize(int64_t n, double* w, const double* h) {
+  const double d = *h;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = d > 0.0 ? w[i] / d : 0.0;
+}
+
+// x = sum_j y_j v_j in basis order    (solver.py:130-133)
+__global__ void k_combine(int64_t n, int m, const double* __restrict__ V, const double* __restrict__ y,
+                          double* x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < m; ++j) acc += y[j] * V[(size_t)j * n + i];
+    x[i] = acc;
+  }
+}
+
+__global__ void k_scale(int64_t n, const double* b, const double* nb, double* v) {
+  const double d = *nb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = b[i] / d;
+}
+
+double relax_eps(double r, double eta) { return std::min(eta / std::min(std::max(r, eta), 1.0), 1.0); }
+
+int schedule_p(double r, double eta, int p_initial, int p_min) {
+  const double eps = relax_eps(r, eta);
+  const int p = eps < 1.0 ? (int)std::ceil(-std::log2(eps)) : p_min;
+  return std::min(p_initial, std::max(p_min, p));
+}
+
+}  // namespace
+
+GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int p_min,
+                     bool relaxed, int max_iter, double* x) {
+  FMM_REQUIRE(tol > 0.0, "eta must be positive");
+  FMM_REQUIRE(max_iter >= 0, "max_iter must be >= 0");
+  FMM_REQUIRE(p_initial >= 0 && p_initial <= P_MAX, "p_initial must be in [0, 20]");
+  GmresResult res;
+  const int64_t n = op.n;
+  cudaStream_t s = op.s_main;
+  DevBuf<double> partials(RB), scal(max_iter + 3);
+  DevBuf<unsigned> counter(1);
+  counter.zero(s);
+  // ||b||
+  double* nb = scal.get() + max_iter + 2;
+  k_norm<<<RB, RT, 0, s>>>(n, const_cast<double*>(b), nullptr, nullptr, partials.get(), counter.get(), nb);
+  FMM_LAUNCH_CHECK();
+  double norm_b = 0.0;
+  FMM_CUDA(cudaMemcpyAsync(&norm_b, nb, sizeof(double), cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  if (norm_b == 0.0) {
+    FMM_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    res.converged = true;
+    return res;
+  }
+  DevBuf<double> V((size_t)(max_iter + 1) * n);
+  k_scale<<<RB, RT, 0, s>>>(n, b, nb, V.get());
+  std::vector<double> H((size_t)(max_iter + 1) * std::max(max_iter, 1), 0.0);
+  auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * max_iter + j]; };
+  std::vector<double> cs(max_iter), sn(max_iter), g(max_iter + 1, 0.0), hcol(max_iter + 2);
+  g[0] = norm_b;
+  double residual = 1.0;
+  int prev_p = p_initial;
+  double* hd = scal.get();  // H column k on device: hd[0..k+1]
+  for (int k = 0; k < max_iter; ++k) {
+    int p = relaxed ? std::min(schedule_p(residual, tol, p_initial, p_min), prev_p) : p_initial;
+    prev_p = p;
+    double* w = V.get() + (size_t)(k + 1) * n;
+    op_apply_device(op, V.get() + (size_t)k * n, w, p);
+    for (int j = 0; j <= k; ++j)
+      k_mgs<<<RB, RT, 0, s>>>(n, V.get() + (size_t)j * n, w, j ? V.get() + (size_t)(j - 1) * n : nullptr,
+                              j ? hd + j - 1 : nullptr, partials.get(), counter.get(), hd + j);
+    k_norm<<<RB, RT, 0, s>>>(n, w, V.get() + (size_t)k * n, hd + k, partials.get(), counter.get(), hd + k + 1);
+    k_normalize<<<RB, RT, 0, s>>>(n, w, hd + k + 1);
+    FMM_LAUNCH_CHECK();
+    FMM_CUDA(cudaMemcpyAsync(hcol.data(), hd, (k + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    for (int j = 0; j <= k + 1; ++j) Hat(j, k) = hcol[j];
+    for (int j = 0; j < k; ++j) {
+      const double h1 = cs[j] * Hat(j, k) + sn[j] * Hat(j + 1, k);
+      Hat(j + 1, k) = -sn[j] * Hat(j, k) + cs[j] * Hat(j + 1, k);
+      Hat(j, k) = h1;
+    }
+    const double denom = std::hypot(Hat(k, k), Hat(k + 1, k));
+    cs[k] = Hat(k, k) / denom;
+    sn[k] = Hat(k + 1, k) / denom;
+    Hat(k, k) = denom;
+    Hat(k + 1, k) = 0.0;
+    g[k + 1] = -sn[k] * g[k];
+    g[k] = cs[k] * g[k];
+    residual = std::fabs(g[k + 1]) / norm_b;
+    res.residuals.push_back(residual);
+    res.orders.push_back(p);
+    if (residual < tol) {
+      res.converged = true;
+      break;
+    }
+  }
+  const int m = (int)res.orders.size();
+  // back substitution on the triangular H[:m,:m] (np.linalg.solve in the reference)
+  std::vector<double> y(std::max(m, 1), 0.0);
+  for (int i = m - 1; i >= 0; --i) {
+    double t = g[i];
+    for (int j = i + 1; j < m; ++j) t -= Hat(i, j) * y[j];
+    y[i] = t / Hat(i, i);
+  }
+  DevBuf<double> yd;
+  yd.upload(y, s);
+  k_combine<<<RB, RT, 0, s>>>(n, m, V.get(), yd.get(), x);
+  FMM_LAUNCH_CHECK();
+  FMM_CUDA(cudaStreamSynchronize(s));
+  return res;
+}
+
+}  // namespace fmmbem

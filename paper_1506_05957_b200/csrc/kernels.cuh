@@ -1,0 +1,57 @@
+// Launch wrappers for the hot-path kernels (one translation unit each).
+#pragma once
+
+#include "plan.cuh"
+
+namespace fmmbem {
+
+// plain-pointer view of a Tree for kernel arguments
+struct TreeDev {
+  const double *px, *py, *pz;
+  const double *cx, *cy, *cz, *half;
+  const int *level, *parent, *first_child, *n_child, *body_start, *body_count, *perm;
+  const uint8_t* is_leaf;
+  int64_t n_points;
+};
+
+inline TreeDev tree_dev(const Tree& t) {
+  return TreeDev{t.px.get(), t.py.get(), t.pz.get(), t.cx.get(), t.cy.get(), t.cz.get(),
+                 t.half.get(), t.level.get(), t.parent.get(), t.first_child.get(),
+                 t.n_child.get(), t.body_start.get(), t.body_count.get(), t.perm.get(),
+                 t.is_leaf.get(), t.n_points};
+}
+
+void upload_index_tables();
+
+// far field
+void launch_p2m(const TreeDev& S, const int* leaves, int n_leaves, int p, int C, const double* q,
+                const double* d, double2* M, cudaStream_t st);
+void launch_m2m(const TreeDev& S, const Tree& host, int p, int C, const double2* rshift,
+                double2* M, cudaStream_t st);
+void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, cudaStream_t st);
+void launch_l2l(const TreeDev& T, const Tree& host, int p, int C, const double2* rshift,
+                double2* L, cudaStream_t st);
+
+// near field (P2P) kinds
+enum class P2PKind : int { LAP_Q = 0, LAP_D = 1, STOKESLET = 2, STRESSLET = 3 };
+inline int p2p_comps(P2PKind k) { return (k == P2PKind::LAP_Q || k == P2PKind::LAP_D) ? 1 : 3; }
+
+// Writes per-item partial sums part[(item.out_off + local_target) * comps + comp].
+// Source strengths (sorted source order): LAP_Q: w[ns]; LAP_D: w[ns*3] dipoles;
+// STOKESLET: w[ns*3] forces; STRESSLET: w[ns*6] = (force, normal).
+void launch_p2p(P2PKind kind, const TreeDev& S, const TreeDev& T, const P2PItem* items,
+                int n_items, const int* p2p_src, int max_sources, const double* w, double* part,
+                cudaStream_t st);
+
+// generic channel near field (FmmPlan.near_field): charges q[C][ns] and/or dipoles d[C][ns][3];
+// accumulates into pot[C][nt] (+ grad[C][nt][3]) in ORIGINAL target order.
+void launch_p2p_channels(const TreeDev& S, const TreeDev& T, const Plan& plan, int C,
+                         const double* q, const double* d, bool want_grad, double* pot,
+                         double* grad, cudaStream_t st);
+
+// generic L2P (FmmPlan.far_field tail): pot[C][nt] (+ grad) in ORIGINAL target order
+void launch_l2p_channels(const TreeDev& T, const int* leaves, int n_leaves, int p, int C,
+                         bool want_grad, const double2* L, double* pot, double* grad,
+                         cudaStream_t st);
+
+}  // namespace fmmbem

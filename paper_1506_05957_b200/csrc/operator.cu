@@ -1,0 +1,522 @@
+// BemOperator.apply / dense_apply / assemble_rhs on device.
+//
+// Reference: BemOperator._layer_apply (bemop.py:192-232), _apply (280-288),
+// assemble_rhs (290-310), _gauss_density (188-190), the Stokes channel maps
+// (fmm.py:422-453).  One layer application is
+//
+//   density gather  ->  [stream B]  P2P items ------------------------------+
+//                   ->  [stream A]  P2M -> M2M -> M2L -> L2L --------------+-> epilogue
+//
+// and the epilogue fuses L2P (+ gradients), the sum of the P2P item
+// partials, the near/singular correction SpMV, the Stokes/stresslet
+// recombination, the 1/(4 pi) or 1/(8 pi mu) factors and the 0.5 x term.
+// apply(x, p) is captured once per p into a CUDA graph and replayed.
+#include "operator.cuh"
+#include "l2p.cuh"
+
+namespace fmmbem {
+
+void upload_index_tables();
+
+namespace {
+
+constexpr double FOUR_PI = 12.566370614359172;
+
+__global__ void k_sorted_sources(int64_t ns, const int* perm, const double* gw, double* s_w,
+                                 int* s_panel) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const int o = perm[i];
+  s_w[i] = gw[o];
+  s_panel[i] = o / 4;  // 4 far-rule points per panel, panel-major (bemop.py:68-70)
+}
+
+// Gauss-point densities w_g * x[panel(g)] in sorted source order (bemop.py:188-190)
+template <int KIND>
+__global__ void k_density(int64_t ns, const double* __restrict__ s_w, const int* __restrict__ s_panel,
+                          const double* __restrict__ px, const double* __restrict__ py,
+                          const double* __restrict__ pz, const double* __restrict__ nrm,
+                          const double* __restrict__ x, double* q, double* dip, double* wsrc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const int pn = s_panel[i];
+  const double w = s_w[i];
+  if (KIND == K_LAP_SINGLE) {
+    q[i] = w * x[pn];
+  } else if (KIND == K_LAP_DOUBLE) {
+    const double v = w * x[pn];
+    dip[3 * i] = v * nrm[3 * pn];
+    dip[3 * i + 1] = v * nrm[3 * pn + 1];
+    dip[3 * i + 2] = v * nrm[3 * pn + 2];
+  } else {
+    const double f0 = w * x[3 * pn], f1 = w * x[3 * pn + 1], f2 = w * x[3 * pn + 2];
+    const double yf = px[i] * f0 + py[i] * f1 + pz[i] * f2;
+    if (KIND == K_STOKESLET) {
+      // channels (f_x, f_y, f_z, y.f) (fmm.py:422-425)
+      q[i] = f0;
+      q[ns + i] = f1;
+      q[2 * ns + i] = f2;
+      q[3 * ns + i] = yf;
+      wsrc[3 * i] = f0;
+      wsrc[3 * i + 1] = f1;
+      wsrc[3 * i + 2] = f2;
+    } else {
+      // seven dipole channels Phi_c = f_c n, Lambda_c = n_c f, Psi = (y.f) n (fmm.py:436-445)
+      const double n0 = nrm[3 * pn], n1 = nrm[3 * pn + 1], n2 = nrm[3 * pn + 2];
+      const double f[3] = {f0, f1, f2}, nn[3] = {n0, n1, n2};
+      for (int c = 0; c < 3; ++c)
+        for (int k = 0; k < 3; ++k) {
+          dip[(c * ns + i) * 3 + k] = f[c] * nn[k];
+          dip[((3 + c) * ns + i) * 3 + k] = nn[c] * f[k];
+        }
+      for (int k = 0; k < 3; ++k) dip[(6 * ns + i) * 3 + k] = yf * nn[k];
+      for (int k = 0; k < 3; ++k) {
+        wsrc[6 * i + k] = f[k];
+        wsrc[6 * i + 3 + k] = nn[k];
+      }
+    }
+  }
+}
+
+template <int KIND> struct EpiTraits;
+template <> struct EpiTraits<K_LAP_SINGLE> { static constexpr int C = 1, NC = 1; static constexpr bool GRAD = false; };
+template <> struct EpiTraits<K_LAP_DOUBLE> { static constexpr int C = 1, NC = 1; static constexpr bool GRAD = false; };
+template <> struct EpiTraits<K_STOKESLET> { static constexpr int C = 4, NC = 3; static constexpr bool GRAD = true; };
+template <> struct EpiTraits<K_STRESSLET> { static constexpr int C = 7, NC = 3; static constexpr bool GRAD = true; };
+
+struct EpiArgs {
+  const int* leaves;
+  const int* item_begin;
+  const P2PItem* items;
+  const double* part;
+  const double2* L;
+  int p;
+  const int* rowptr;
+  const int* cols;
+  const double* vals;
+  const double* x;
+  double alpha, beta;
+  double* y;
+};
+
+template <int KIND, bool FAR>
+__global__ void __launch_bounds__(128) k_epilogue(TreeDev T, EpiArgs a) {
+  using Tr = EpiTraits<KIND>;
+  constexpr int C = Tr::C, NC = Tr::NC;
+  extern __shared__ double2 sL[];
+  const int li = blockIdx.x;
+  const int leaf = a.leaves[li];
+  const int H = hcount(a.p);
+  if (FAR) {
+    for (int i = threadIdx.x; i < C * H; i += blockDim.x) sL[i] = a.L[(size_t)leaf * C * H + i];
+    __syncthreads();
+  }
+  const int t0 = T.body_start[leaf], nt = T.body_count[leaf];
+  const double cx = T.cx[leaf], cy = T.cy[leaf], cz = T.cz[leaf];
+  const int ib = a.item_begin[li], ie = a.item_begin[li + 1];
+  for (int lt = threadIdx.x; lt < nt; lt += blockDim.x) {
+    const int ti = t0 + lt;
+    const int pn = T.perm[ti];
+    double near[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) near[c] = 0.0;
+    for (int it = ib; it < ie; ++it) {
+      const double* pp = a.part + (size_t)(a.items[it].out_off + lt) * NC;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) near[c] += pp[c];
+    }
+    const double tx = T.px[ti], ty = T.py[ti], tz = T.pz[ti];
+    double pot[C], grad[3 * C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) { pot[c] = 0.0; grad[3 * c] = grad[3 * c + 1] = grad[3 * c + 2] = 0.0; }
+    if (FAR) l2p_eval<C, Tr::GRAD>(sL, H, a.p, tx - cx, ty - cy, tz - cz, pot, grad);
+    if (KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) {
+      double corr = 0.0;
+      for (int e = a.rowptr[pn]; e < a.rowptr[pn + 1]; ++e) corr = fma(a.vals[e], a.x[a.cols[e]], corr);
+      const double layer = (pot[0] + near[0]) / FOUR_PI + corr;
+      a.y[pn] = a.alpha * a.x[pn] + a.beta * layer;
+    } else {
+      const double xt[3] = {tx, ty, tz};
+      double u[3];
+      for (int i = 0; i < 3; ++i) {
+        if (KIND == K_STOKESLET) {
+          // u_i = phi_i - x_c d_i phi_c + d_i psi (fmm.py:428-433)
+          double v = pot[i];
+          for (int c = 0; c < 3; ++c) v -= xt[c] * grad[3 * c + i];
+          u[i] = v + grad[3 * 3 + i];
+        } else {
+          // u_i = 2 Lambda_i - 2 x_c d_i Phi_c + 2 d_i Psi (fmm.py:448-453)
+          double v = 2.0 * pot[3 + i];
+          for (int c = 0; c < 3; ++c) v -= 2.0 * xt[c] * grad[3 * c + i];
+          u[i] = v + 2.0 * grad[3 * 6 + i];
+        }
+        u[i] += near[i];
+      }
+      double corr[3] = {0.0, 0.0, 0.0};
+      for (int e = a.rowptr[pn]; e < a.rowptr[pn + 1]; ++e) {
+        const double* blk = a.vals + (size_t)e * 9;
+        const double* xs = a.x + 3 * (size_t)a.cols[e];
+        for (int r = 0; r < 3; ++r)
+          corr[r] = fma(blk[3 * r], xs[0], fma(blk[3 * r + 1], xs[1], fma(blk[3 * r + 2], xs[2], corr[r])));
+      }
+      for (int r = 0; r < 3; ++r)
+        a.y[3 * pn + r] = a.alpha * a.x[3 * pn + r] + a.beta * (u[r] + corr[r]);
+    }
+  }
+}
+
+template <int KIND>
+void launch_density(BemOp& op, const double* x, cudaStream_t s) {
+  const int64_t ns = op.plan.src.n_points;
+  k_density<KIND><<<grid_for(ns, 256), 256, 0, s>>>(
+      ns, op.s_weight.get(), op.s_panel.get(), op.plan.src.px.get(), op.plan.src.py.get(),
+      op.plan.src.pz.get(), op.normal.get(), x, op.q.get(), op.dip.get(), op.wsrc.get());
+  FMM_LAUNCH_CHECK();
+}
+
+template <int KIND>
+void launch_epilogue(BemOp& op, const EpiArgs& a, bool far, cudaStream_t s) {
+  constexpr int C = EpiTraits<KIND>::C;
+  const size_t smem = far ? (size_t)C * hcount(a.p) * sizeof(double2) : 0;
+  const int nl = op.plan.tgt.n_leaves;
+  if (far) {
+    FMM_CUDA(cudaFuncSetAttribute(k_epilogue<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(C * hcount(P_MAX) * sizeof(double2))));
+    k_epilogue<KIND, true><<<nl, 128, smem, s>>>(tree_dev(op.plan.tgt), a);
+  } else {
+    k_epilogue<KIND, false><<<nl, 128, 0, s>>>(tree_dev(op.plan.tgt), a);
+  }
+  FMM_LAUNCH_CHECK();
+}
+
+int layer_channels(int kind) { return kind == K_STOKESLET ? 4 : kind == K_STRESSLET ? 7 : 1; }
+
+void ensure_dense(BemOp& op) {
+  if (op.dense_ready) return;
+  std::vector<int> row, srcl, ib;
+  plan_dense_items(op.plan, op.dense_items_h, row, srcl, ib, op.dense_part_len);
+  op.dense_items.upload(op.dense_items_h);
+  op.dense_src.upload(srcl);
+  op.dense_item_begin.upload(ib);
+  op.dense_max_sources = 0;
+  for (const auto& it : op.dense_items_h) {
+    int acc = 0;
+    for (int k = it.pair_begin; k < it.pair_end; ++k) acc += op.plan.src.h_body_count[srcl[k]];
+    op.dense_max_sources = std::max(op.dense_max_sources, acc);
+  }
+  FMM_CUDA(cudaDeviceSynchronize());
+  op.dense_ready = true;
+}
+
+void clear_graphs(BemOp& op) {
+  for (auto& kv : op.graphs) cudaGraphExecDestroy(kv.second);
+  op.graphs.clear();
+}
+
+// allocations and p-dependent tables; never called inside a stream capture.
+void prepare(BemOp& op, int kind, int p, bool dense) {
+  FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p must be in [0, 20]");
+
+  const int C = layer_channels(kind);
+  const int64_t ns = op.plan.src.n_points;
+  op.q.ensure((size_t)ns * (kind == K_STOKESLET ? 4 : 1));
+  op.dip.ensure((size_t)ns * 3 * (kind == K_STRESSLET ? 7 : 1));
+  op.wsrc.ensure((size_t)ns * 6);
+  if (dense) {
+    ensure_dense(op);
+    op.part_dense.ensure((size_t)std::max<int64_t>(op.dense_part_len, 1) * 3);
+  } else {
+    op.part.ensure((size_t)std::max<int64_t>(op.plan.part_len, 1) * 3);
+    op.M.ensure((size_t)op.plan.src.n_cells * C * hcount(p));
+    op.L.ensure((size_t)op.plan.tgt.n_cells * C * hcount(p));
+    plan_ensure_igrid(op.plan, p, op.s_main);
+  }
+}
+
+void record(BemOp& op, int stage, bool end, cudaStream_t s) {
+  if (op.timing) FMM_CUDA(cudaEventRecord(op.ev[2 * stage + (end ? 1 : 0)], s));
+}
+
+}  // namespace
+
+BemOp::~BemOp() {
+  for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (s_main) cudaStreamDestroy(s_main);
+  if (s_near) cudaStreamDestroy(s_near);
+}
+
+void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* gauss_pts,
+             const double* gauss_wts, const double* fine_pts, const double* fine_wts,
+             const double* normals, const double* areas, const double* leg_x, const double* leg_w,
+             int n_gauss_singular, int formulation, double theta, int n_crit, double mu,
+             double near_factor, int max_depth) {
+  FMM_REQUIRE(P > 0, "mesh must have panels");
+  FMM_REQUIRE(formulation >= 0 && formulation <= 2, "unknown formulation");
+  FMM_REQUIRE(n_gauss_singular >= 1, "n_gauss_singular must be >= 1");
+  upload_index_tables();
+  op.formulation = formulation;
+  op.mu = mu;
+  op.near_factor = near_factor;
+  op.n_gauss_singular = n_gauss_singular;
+  op.n_panels = P;
+  op.n = formulation == STOKES ? 3 * P : P;
+  FMM_CUDA(cudaStreamCreateWithFlags(&op.s_main, cudaStreamNonBlocking));
+  FMM_CUDA(cudaStreamCreateWithFlags(&op.s_near, cudaStreamNonBlocking));
+  FMM_CUDA(cudaEventCreateWithFlags(&op.ev_fork, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&op.ev_join, cudaEventDisableTiming));
+  for (auto& e : op.ev) FMM_CUDA(cudaEventCreate(&e));
+  cudaStream_t s = op.s_main;
+  // collocation points are bitwise the centroid Gauss point (bemop.py:64-67)
+  std::vector<double> cen(3 * P);
+  for (int64_t j = 0; j < P; ++j)
+    for (int d = 0; d < 3; ++d) cen[3 * j + d] = gauss_pts[12 * j + d];
+  op.centroid.upload(cen, s);
+  op.normal.upload(normals, 3 * P, s);
+  op.area.upload(areas, P, s);
+  op.panel_verts.upload(panel_vertices, 9 * P, s);
+  op.gauss_pos.upload(gauss_pts, 12 * P, s);
+  op.gauss_w.upload(gauss_wts, 4 * P, s);
+  op.fine_pos.upload(fine_pts, 57 * P, s);
+  op.fine_w.upload(fine_wts, 19 * P, s);
+  op.leg_x.upload(leg_x, n_gauss_singular, s);
+  op.leg_w.upload(leg_w, n_gauss_singular, s);
+  plan_build(op.plan, gauss_pts, 4 * P, cen.data(), P, n_crit, theta, max_depth, s);
+  const int64_t ns = op.plan.src.n_points;
+  op.s_weight.resize(ns);
+  op.s_panel.resize(ns);
+  k_sorted_sources<<<grid_for(ns, 256), 256, 0, s>>>(ns, op.plan.src.perm.get(), op.gauss_w.get(),
+                                                      op.s_weight.get(), op.s_panel.get());
+  FMM_LAUNCH_CHECK();
+  op.max_item_sources = 0;
+  for (const auto& it : op.plan.items) {
+    int acc = 0;
+    for (int k = it.pair_begin; k < it.pair_end; ++k) acc += op.plan.src.h_body_count[op.plan.h_p2p_src[k]];
+    op.max_item_sources = std::max(op.max_item_sources, acc);
+  }
+  build_near_pairs(op, s);
+  int sys_kind, rhs_kind;
+  if (formulation == LAPLACE_FIRST) { sys_kind = K_LAP_SINGLE; rhs_kind = K_LAP_DOUBLE; }
+  else if (formulation == LAPLACE_SECOND) { sys_kind = K_LAP_DOUBLE; rhs_kind = K_LAP_SINGLE; }
+  else { sys_kind = K_STOKESLET; rhs_kind = K_STRESSLET; }
+  build_correction(op, sys_kind, op.c_sys, s);
+  build_correction(op, rhs_kind, op.c_rhs, s);
+  op.x_in.resize(op.n);
+  op.y_out.resize(op.n);
+  // size the apply workspaces for the largest order up front (graphs bake in addresses)
+  prepare(op, sys_kind, P_MAX, false);
+  FMM_CUDA(cudaStreamSynchronize(s));
+}
+
+void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s) {
+  Plan& pl = op.plan;
+  const int C = layer_channels(c.kind);
+  const TreeDev S = tree_dev(pl.src), T = tree_dev(pl.tgt);
+  record(op, ST_TOTAL, false, s);
+  switch (c.kind) {
+    case K_LAP_SINGLE: launch_density<K_LAP_SINGLE>(op, c.x, s); break;
+    case K_LAP_DOUBLE: launch_density<K_LAP_DOUBLE>(op, c.x, s); break;
+    case K_STOKESLET: launch_density<K_STOKESLET>(op, c.x, s); break;
+    default: launch_density<K_STRESSLET>(op, c.x, s); break;
+  }
+  const double* w = c.kind == K_LAP_SINGLE ? op.q.get() : c.kind == K_LAP_DOUBLE ? op.dip.get()
+                                                                                : op.wsrc.get();
+  // near field on the second stream
+  FMM_CUDA(cudaEventRecord(op.ev_fork, s));
+  FMM_CUDA(cudaStreamWaitEvent(op.s_near, op.ev_fork, 0));
+  record(op, ST_P2P, false, op.s_near);
+  if (c.dense)
+    launch_p2p((P2PKind)c.kind, S, T, op.dense_items.get(), (int)op.dense_items_h.size(),
+               op.dense_src.get(), op.dense_max_sources, w, op.part_dense.get(), op.s_near);
+  else
+    launch_p2p((P2PKind)c.kind, S, T, pl.d_items.get(), (int)pl.items.size(), pl.p2p_src.get(),
+               op.max_item_sources, w, op.part.get(), op.s_near);
+  record(op, ST_P2P, true, op.s_near);
+  FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
+  // far field on the main stream
+  if (!c.dense) {
+    const double* q = (c.kind == K_LAP_SINGLE || c.kind == K_STOKESLET) ? op.q.get() : nullptr;
+    const double* d = (c.kind == K_LAP_DOUBLE || c.kind == K_STRESSLET) ? op.dip.get() : nullptr;
+    record(op, ST_UP, false, s);
+    launch_p2m(S, pl.src.leaves.get(), pl.src.n_leaves, c.p, C, q, d, op.M.get(), s);
+    launch_m2m(S, pl.src, c.p, C, pl.rshift_src.get(), op.M.get(), s);
+    record(op, ST_UP, true, s);
+    FMM_CUDA(cudaMemsetAsync(op.L.get(), 0, (size_t)pl.tgt.n_cells * C * hcount(c.p) * sizeof(double2), s));
+    record(op, ST_M2L, false, s);
+    launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), s);
+    record(op, ST_M2L, true, s);
+    record(op, ST_DOWN, false, s);
+    launch_l2l(T, pl.tgt, c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
+    record(op, ST_DOWN, true, s);
+  }
+  FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
+  EpiArgs a;
+  a.leaves = pl.tgt.leaves.get();
+  a.item_begin = c.dense ? op.dense_item_begin.get() : pl.tleaf_item_begin.get();
+  a.items = c.dense ? op.dense_items.get() : pl.d_items.get();
+  a.part = c.dense ? op.part_dense.get() : op.part.get();
+  a.L = op.L.get();
+  a.p = c.p;
+  a.rowptr = op.near_rowptr.get();
+  a.cols = op.near_cols.get();
+  a.vals = c.corr->vals.get();
+  a.x = c.x;
+  a.alpha = c.alpha;
+  a.beta = c.beta;
+  a.y = c.y;
+  record(op, ST_EPI, false, s);
+  switch (c.kind) {
+    case K_LAP_SINGLE: launch_epilogue<K_LAP_SINGLE>(op, a, !c.dense, s); break;
+    case K_LAP_DOUBLE: launch_epilogue<K_LAP_DOUBLE>(op, a, !c.dense, s); break;
+    case K_STOKESLET: launch_epilogue<K_STOKESLET>(op, a, !c.dense, s); break;
+    default: launch_epilogue<K_STRESSLET>(op, a, !c.dense, s); break;
+  }
+  record(op, ST_EPI, true, s);
+  record(op, ST_TOTAL, true, s);
+}
+
+namespace {
+
+void sys_call(BemOp& op, int p, bool dense, const double* x, double* y, LayerCall& c) {
+  c.p = p;
+  c.dense = dense;
+  c.corr = &op.c_sys;
+  c.x = x;
+  c.y = y;
+  if (op.formulation == LAPLACE_FIRST) { c.kind = K_LAP_SINGLE; c.alpha = 0.0; c.beta = 1.0; }
+  else if (op.formulation == LAPLACE_SECOND) { c.kind = K_LAP_DOUBLE; c.alpha = 0.5; c.beta = -1.0; }
+  else { c.kind = K_STOKESLET; c.alpha = 0.0; c.beta = 1.0 / (8.0 * 3.141592653589793 * op.mu); }
+}
+
+void accumulate_stage_times(BemOp& op) {
+  if (!op.timing) return;
+  FMM_CUDA(cudaStreamSynchronize(op.s_main));
+  for (int st = 0; st < N_STAGES; ++st) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, op.ev[2 * st], op.ev[2 * st + 1]) == cudaSuccess)
+      op.stage_ms[st] += ms;
+    else
+      cudaGetLastError();
+  }
+  op.stage_calls++;
+}
+
+}  // namespace
+
+// y = A x for device vectors (x, y may alias nothing in the op)
+void op_apply_device(BemOp& op, const double* x, double* y, int p) {
+  LayerCall c;
+  sys_call(op, p, false, op.x_in.get(), op.y_out.get(), c);
+  prepare(op, c.kind, p, false);
+  cudaStream_t s = op.s_main;
+  FMM_CUDA(cudaMemcpyAsync(op.x_in.get(), x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (op.use_graphs) {
+    // captured graphs bake in buffer addresses: any reallocation invalidates them
+    const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
+                                          op.M.get(), op.L.get(), op.plan.igrid.get(),
+                                          op.x_in.get(), op.y_out.get()};
+    if (sig != op.graph_sig) {
+      clear_graphs(op);
+      op.graph_sig = sig;
+    }
+    const int key = p * 2 + (op.timing ? 1 : 0);
+    auto it = op.graphs.find(key);
+    if (it == op.graphs.end()) {
+      cudaGraph_t g;
+      FMM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      try {
+        op_layer(op, c, s);
+      } catch (...) {
+        cudaStreamEndCapture(s, &g);
+        throw;
+      }
+      FMM_CUDA(cudaStreamEndCapture(s, &g));
+      cudaGraphExec_t ex;
+      FMM_CUDA(cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      it = op.graphs.emplace(key, ex).first;
+    }
+    FMM_CUDA(cudaGraphLaunch(it->second, s));
+  } else {
+    op_layer(op, c, s);
+  }
+  FMM_CUDA(cudaMemcpyAsync(y, op.y_out.get(), op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  accumulate_stage_times(op);
+}
+
+void op_dense_apply_device(BemOp& op, const double* x, double* y) {
+  LayerCall c;
+  sys_call(op, 0, true, x, y, c);
+  prepare(op, c.kind, 0, true);
+  op_layer(op, c, op.s_main);
+  FMM_CUDA(cudaStreamSynchronize(op.s_main));
+}
+
+void op_rhs_device(BemOp& op, const double* data, double* b, int p, bool dense) {
+  LayerCall c;
+  c.p = p;
+  c.dense = dense;
+  c.corr = &op.c_rhs;
+  c.x = data;
+  c.y = b;
+  if (op.formulation == LAPLACE_FIRST) { c.kind = K_LAP_DOUBLE; c.alpha = 0.5; c.beta = -1.0; }
+  else if (op.formulation == LAPLACE_SECOND) { c.kind = K_LAP_SINGLE; c.alpha = 0.0; c.beta = 1.0; }
+  else { c.kind = K_STRESSLET; c.alpha = 0.5; c.beta = -1.0 / (8.0 * 3.141592653589793); }
+  prepare(op, c.kind, p, dense);
+  op_layer(op, c, op.s_main);
+  FMM_CUDA(cudaStreamSynchronize(op.s_main));
+}
+
+// ------------------------------------------------------- FmmPlan far/near (generic)
+namespace {
+__global__ void k_permute_channels(int64_t ns, int C, int width, const int* perm, const double* in,
+                                   double* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const int o = perm[i];
+  for (int c = 0; c < C; ++c)
+    for (int k = 0; k < width; ++k) out[((size_t)c * ns + i) * width + k] = in[((size_t)c * ns + o) * width + k];
+}
+}  // namespace
+
+void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig, int p,
+                   bool want_grad, int parts, double* pot, double* grad, cudaStream_t s) {
+  upload_index_tables();
+  FMM_REQUIRE(C == 1 || C == 4 || C == 7, "channel count must be 1, 4 or 7");
+  FMM_REQUIRE(q_orig || d_orig, "charges or dipoles required");
+  const int64_t ns = plan.src.n_points;
+  DevBuf<double> qs, ds;
+  if (q_orig) {
+    qs.resize((size_t)C * ns);
+    k_permute_channels<<<grid_for(ns, 256), 256, 0, s>>>(ns, C, 1, plan.src.perm.get(), q_orig, qs.get());
+  }
+  if (d_orig) {
+    ds.resize((size_t)C * ns * 3);
+    k_permute_channels<<<grid_for(ns, 256), 256, 0, s>>>(ns, C, 3, plan.src.perm.get(), d_orig, ds.get());
+  }
+  FMM_LAUNCH_CHECK();
+  const TreeDev S = tree_dev(plan.src), T = tree_dev(plan.tgt);
+  if (parts & 1) {
+    plan_ensure_igrid(plan, p, s);
+    DevBuf<double2> M((size_t)plan.src.n_cells * C * hcount(p)), L((size_t)plan.tgt.n_cells * C * hcount(p));
+    L.zero(s);
+    launch_p2m(S, plan.src.leaves.get(), plan.src.n_leaves, p, C, q_orig ? qs.get() : nullptr,
+               d_orig ? ds.get() : nullptr, M.get(), s);
+    launch_m2m(S, plan.src, p, C, plan.rshift_src.get(), M.get(), s);
+    launch_m2l(plan, p, C, M.get(), L.get(), s);
+    launch_l2l(T, plan.tgt, p, C, plan.rshift_tgt.get(), L.get(), s);
+    launch_l2p_channels(T, plan.tgt.leaves.get(), plan.tgt.n_leaves, p, C, want_grad, L.get(), pot,
+                        grad, s);
+    FMM_CUDA(cudaStreamSynchronize(s));
+  }
+  if (parts & 2) {
+    launch_p2p_channels(S, T, plan, C, q_orig ? qs.get() : nullptr, d_orig ? ds.get() : nullptr,
+                        want_grad, pot, grad, s);
+  }
+  FMM_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace fmmbem

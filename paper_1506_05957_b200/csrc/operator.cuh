@@ -1,0 +1,108 @@
+// BemOperator on device: plan + geometry + corrections + apply/GMRES.
+#pragma once
+
+#include <map>
+#include <memory>
+
+#include "kernels.cuh"
+
+namespace fmmbem {
+
+enum Formulation : int { LAPLACE_FIRST = 0, LAPLACE_SECOND = 1, STOKES = 2 };
+// layer kernels, numbered like P2PKind
+enum LayerKind : int { K_LAP_SINGLE = 0, K_LAP_DOUBLE = 1, K_STOKESLET = 2, K_STRESSLET = 3 };
+
+struct Correction {
+  int kind = -1;
+  int block = 1;          // 1 (scalar) or 9 (3x3 block, row-major)
+  DevBuf<double> vals;    // near_nnz * block
+};
+
+// stage timers captured with the apply (CUDA events on the launching streams)
+enum Stage : int { ST_P2P = 0, ST_UP = 1, ST_M2L = 2, ST_DOWN = 3, ST_EPI = 4, ST_TOTAL = 5, N_STAGES = 6 };
+
+struct BemOp {
+  int formulation = LAPLACE_SECOND;
+  double mu = 1e-3;
+  double near_factor = 2.0;
+  int n_gauss_singular = 32;
+  int64_t n_panels = 0;
+  int64_t n = 0;  // unknowns
+  int device = 0;
+  Plan plan;
+  cudaStream_t s_main = nullptr, s_near = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
+  // geometry, panel order
+  DevBuf<double> centroid, normal, area, panel_verts, gauss_pos, gauss_w, fine_pos, fine_w;
+  DevBuf<double> leg_x, leg_w;
+  // per sorted source: weight, panel, absolute position is plan.src.p{x,y,z}
+  DevBuf<double> s_weight;
+  DevBuf<int> s_panel;
+
+  // near pairs (CSR by target panel) and the two corrections
+  int near_nnz = 0;
+  DevBuf<int> near_rowptr, near_cols;
+  Correction c_sys, c_rhs;
+
+  // work buffers
+  DevBuf<double> x_in, y_out, q, dip, wsrc, part, part_dense, stage_x, stage_y;
+  DevBuf<double2> M, L;
+  int max_item_sources = 0;
+  // dense (direct) P2P lists
+  bool dense_ready = false;
+  std::vector<P2PItem> dense_items_h;
+  DevBuf<P2PItem> dense_items;
+  DevBuf<int> dense_src, dense_item_begin;
+  int64_t dense_part_len = 0;
+  int dense_max_sources = 0;
+
+  // CUDA graphs of apply(p), one per order
+  std::map<int, cudaGraphExec_t> graphs;
+  std::vector<const void*> graph_sig;
+  bool use_graphs = true;
+
+  // stage timing
+  bool timing = false;
+  cudaEvent_t ev[2 * N_STAGES] = {};
+  double stage_ms[N_STAGES] = {};
+  int64_t stage_calls = 0;
+
+  ~BemOp();
+};
+
+struct LayerCall {
+  int kind;             // LayerKind
+  int p;
+  bool dense;
+  const Correction* corr;
+  double alpha, beta;   // y = alpha * x + beta * layer(x)
+  const double* x;      // device, panel order (n)
+  double* y;            // device (n)
+};
+
+void op_init(BemOp& op, const double* panel_vertices, int64_t n_panels, const double* gauss_pts,
+             const double* gauss_wts, const double* fine_pts, const double* fine_wts,
+             const double* normals, const double* areas, const double* leg_x, const double* leg_w,
+             int n_gauss_singular, int formulation, double theta, int n_crit, double mu,
+             double near_factor, int max_depth);
+void op_layer(BemOp& op, const LayerCall& call, cudaStream_t s);
+void op_apply_device(BemOp& op, const double* x, double* y, int p);
+void op_dense_apply_device(BemOp& op, const double* x, double* y);
+void op_rhs_device(BemOp& op, const double* data, double* b, int p, bool dense);
+void build_near_pairs(BemOp& op, cudaStream_t s);
+void build_correction(BemOp& op, int kind, Correction& out, cudaStream_t s);
+
+struct GmresResult {
+  std::vector<double> residuals;
+  std::vector<int> orders;
+  bool converged = false;
+};
+GmresResult op_gmres(BemOp& op, const double* b_dev, double tol, int p_initial, int p_min,
+                     bool relaxed, int max_iter, double* x_dev);
+
+// FmmPlan.far_field / near_field (generic channels, host-facing helper)
+void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig, int p,
+                   bool want_grad, int parts, double* pot, double* grad, cudaStream_t s);
+
+}  // namespace fmmbem

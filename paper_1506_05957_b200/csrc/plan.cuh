@@ -1,0 +1,97 @@
+// Octree + dual-traversal plan, resident in HBM.
+//
+// Replaces FmmPlan.__init__ (pkg/src/fmmbem/fmm.py:131-168), build_tree
+// (octree.py:57-131), bounding_cube (octree.py:46-54) and dual_traversal
+// (fmm.py:84-125).  Cells are numbered level by level and in Morton order
+// inside a level (the reference numbers them depth-first); trees and pair
+// sets are compared with the reference by content, never by index.
+#pragma once
+
+#include "common.cuh"
+
+namespace fmmbem {
+
+struct Tree {
+  int64_t n_points = 0;
+  int n_cells = 0;
+  int n_levels = 0;  // levels present: 0 .. n_levels-1
+  int n_leaves = 0;
+  int max_leaf_count = 0;
+  std::vector<int> level_start;  // host: cells of level l are [level_start[l], level_start[l+1])
+  std::vector<double> level_half;  // host: half width per level (root_half * 0.5^l)
+
+  // per cell (device)
+  DevBuf<double> cx, cy, cz, half;
+  DevBuf<int> level, parent, first_child, n_child, body_start, body_count;
+  DevBuf<uint8_t> is_leaf;
+  // leaves in body order (device) and per sorted body its leaf cell
+  DevBuf<int> leaves, leaf_of_body;
+  // sorted position -> original index, and sorted coordinates
+  DevBuf<int> perm;
+  DevBuf<double> px, py, pz;
+
+  // host mirrors (small)
+  std::vector<int> h_level, h_parent, h_first_child, h_n_child, h_body_start, h_body_count;
+  std::vector<uint8_t> h_is_leaf;
+  std::vector<int> h_leaves;
+  std::vector<double> h_cx, h_cy, h_cz;
+};
+
+struct P2PItem {
+  int tgt_leaf;   // target cell id
+  int pair_begin; // range into p2p source-leaf list (CSR of the target leaf)
+  int pair_end;
+  int out_off;    // offset into the per-item partial buffer (in targets)
+};
+
+struct Plan {
+  int device = 0;
+  int n_crit = 0;
+  int max_depth = 20;
+  double theta = 0.5;
+  double root_c[3] = {0, 0, 0};
+  double root_half = 0;
+  Tree src, tgt;
+
+  // M2L: CSR by target cell over (source cell, offset id)
+  int n_m2l = 0;
+  DevBuf<int> m2l_row;     // n_tgt_cells + 1
+  DevBuf<int> m2l_src;     // n_m2l
+  DevBuf<int> m2l_off;     // n_m2l, offset-table index
+  std::vector<int> h_m2l_row, h_m2l_src;
+  int n_offsets = 0;
+  DevBuf<double> off_d;    // 3 * n_offsets, the (lattice-exact) translation vectors
+  DevBuf<double2> igrid;   // n_offsets * hcount(2 * igrid_p)
+  int igrid_p = -1;        // I tables hold orders up to 2 * igrid_p
+  std::vector<int> m2l_tgt_cells;  // target cells with >= 1 M2L source
+  DevBuf<int> d_m2l_tgt_cells;
+
+  // P2P: CSR by target leaf (cell id) over source leaves
+  int n_p2p = 0;
+  DevBuf<int> p2p_row;     // n_tgt_cells + 1
+  DevBuf<int> p2p_src;
+  std::vector<int> h_p2p_row, h_p2p_src;
+  std::vector<P2PItem> items;
+  DevBuf<P2PItem> d_items;
+  DevBuf<int> tleaf_item_begin;  // per target leaf index (body order) -> first item; n_leaves + 1
+  int64_t part_len = 0;          // total targets over items
+  int64_t p2p_interactions = 0;
+
+  // M2M / L2L translation tables: R(d) for the 8 child octants of every level, up to igrid... P_MAX
+  DevBuf<double2> rshift_src;  // [level][octant][hcount(P_MAX)]
+  DevBuf<double2> rshift_tgt;
+};
+
+// builds both trees over a shared root cube, the traversal, and the work lists
+void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt_xyz, int64_t nt,
+                int n_crit, double theta, int max_depth, cudaStream_t s);
+// (re)build the irregular-harmonic tables for M2L up to order 2p
+void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s);
+// dense "every source leaf for every target leaf" item list (dense_apply)
+void plan_dense_items(const Plan& plan, std::vector<P2PItem>& items, std::vector<int>& row,
+                      std::vector<int>& src, std::vector<int>& item_begin, int64_t& part_len);
+void plan_make_items(const Tree& tgt, const Tree& src, const std::vector<int>& row,
+                     const std::vector<int>& srcl, int chunk, std::vector<P2PItem>& items,
+                     std::vector<int>& item_begin, int64_t& part_len, int64_t& interactions);
+
+}  // namespace fmmbem

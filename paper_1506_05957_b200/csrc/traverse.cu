@@ -1,0 +1,284 @@
+// Dual-tree traversal on device, plus the per-apply work lists.
+//
+// Reference: dual_traversal (fmm.py:84-125).  A (source, target) cell pair is
+// accepted for M2L when d > 0 and (r_s + r_t) < theta * d with r = half width
+// (CELL_RADIUS_FACTOR = 1, fmm.py:26); otherwise leaf-leaf pairs go to P2P and
+// the source is split iff it is internal and (the target is a leaf or
+// hw_s >= hw_t) (fmm.py:117).  The reference walks a stack; here the frontier
+// is expanded level-synchronously on the GPU, which yields the same pair sets.
+// Pairs are then sorted by (target, source) so every later accumulation has
+// a fixed order (bitwise-reproducible mat-vecs).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <tuple>
+
+#include "plan.cuh"
+
+namespace fmmbem {
+
+void build_trees(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt_xyz, int64_t nt,
+                 cudaStream_t s);
+
+namespace {
+
+struct TreeView {
+  const double *cx, *cy, *cz, *half;
+  const uint8_t* is_leaf;
+  const int *first_child, *n_child;
+};
+
+TreeView view(const Tree& t) {
+  return TreeView{t.cx.get(), t.cy.get(), t.cz.get(), t.half.get(), t.is_leaf.get(),
+                  t.first_child.get(), t.n_child.get()};
+}
+
+__global__ void k_traverse(const int2* front, int nf, TreeView S, TreeView T, double theta,
+                           int2* next, int* n_next, int2* m2l, int* n_m2l, int2* p2p, int* n_p2p) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nf) return;
+  const int s = front[i].x, t = front[i].y;
+  const double dx = __dadd_rn(S.cx[s], -T.cx[t]);
+  const double dy = __dadd_rn(S.cy[s], -T.cy[t]);
+  const double dz = __dadd_rn(S.cz[s], -T.cz[t]);
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  const double d = sqrt(d2);
+  const double rs = S.half[s], rt = T.half[t];
+  if (d > 0.0 && __dadd_rn(rs, rt) < __dmul_rn(theta, d)) {
+    int k = atomicAdd(n_m2l, 1);
+    m2l[k] = make_int2(s, t);
+    return;
+  }
+  const bool sl = S.is_leaf[s], tl = T.is_leaf[t];
+  if (sl && tl) {
+    int k = atomicAdd(n_p2p, 1);
+    p2p[k] = make_int2(s, t);
+    return;
+  }
+  const bool split_src = !sl && (tl || rs >= rt);
+  if (split_src) {
+    const int f = S.first_child[s], nc = S.n_child[s];
+    int k = atomicAdd(n_next, nc);
+    for (int c = 0; c < nc; ++c) next[k + c] = make_int2(f + c, t);
+  } else {
+    const int f = T.first_child[t], nc = T.n_child[t];
+    int k = atomicAdd(n_next, nc);
+    for (int c = 0; c < nc; ++c) next[k + c] = make_int2(s, f + c);
+  }
+}
+
+void sort_pairs_tgt_major(std::vector<int2>& v) {
+  std::sort(v.begin(), v.end(), [](const int2& a, const int2& b) {
+    return a.y != b.y ? a.y < b.y : a.x < b.x;
+  });
+}
+
+void traverse(Plan& plan, std::vector<int2>& m2l, std::vector<int2>& p2p, cudaStream_t s) {
+  const int B = 256;
+  TreeView S = view(plan.src), T = view(plan.tgt);
+  std::vector<int2> front_h(1, make_int2(0, 0));
+  DevBuf<int2> front, next, dm2l, dp2p;
+  DevBuf<int> counters(3);
+  front.upload(front_h, s);
+  int nf = 1;
+  while (nf > 0) {
+    next.ensure((size_t)nf * 8);
+    dm2l.ensure(nf);
+    dp2p.ensure(nf);
+    counters.zero(s);
+    k_traverse<<<grid_for(nf, B), B, 0, s>>>(front.get(), nf, S, T, plan.theta, next.get(),
+                                             counters.get(), dm2l.get(), counters.get() + 1,
+                                             dp2p.get(), counters.get() + 2);
+    FMM_LAUNCH_CHECK();
+    int c[3];
+    FMM_CUDA(cudaMemcpyAsync(c, counters.get(), sizeof(c), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    if (c[1]) {
+      size_t o = m2l.size();
+      m2l.resize(o + c[1]);
+      FMM_CUDA(cudaMemcpy(m2l.data() + o, dm2l.get(), c[1] * sizeof(int2), cudaMemcpyDeviceToHost));
+    }
+    if (c[2]) {
+      size_t o = p2p.size();
+      p2p.resize(o + c[2]);
+      FMM_CUDA(cudaMemcpy(p2p.data() + o, dp2p.get(), c[2] * sizeof(int2), cudaMemcpyDeviceToHost));
+    }
+    std::swap(front, next);
+    nf = c[0];
+  }
+  sort_pairs_tgt_major(m2l);
+  sort_pairs_tgt_major(p2p);
+}
+
+// I_n^m(D) for every distinct M2L offset, orders n <= 2p, half storage
+__global__ void k_igrid(const double* off, int n_off, int order, double2* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_off) return;
+  irregular_half(off[3 * i], off[3 * i + 1], off[3 * i + 2], order, out + (size_t)i * hcount(order));
+}
+
+// R_n^m(d) for the 8 child offsets (+-h, +-h, +-h) of every level (M2M/L2L operators)
+__global__ void k_rshift(const double* child_half, int n_levels, double2* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_levels * 8) return;
+  const int l = i / 8, o = i % 8;
+  const double h = child_half[l];
+  regular_half((o & 1) ? h : -h, (o & 2) ? h : -h, (o & 4) ? h : -h, P_MAX,
+               out + (size_t)i * hcount(P_MAX));
+}
+
+void build_rshift(const Tree& t, DevBuf<double2>& out, cudaStream_t s) {
+  // entry l holds offsets of level-l cells from their parent: half width of level l
+  std::vector<double> ch(std::max(t.n_levels, 1));
+  for (int l = 0; l < t.n_levels; ++l) ch[l] = t.level_half[l];
+  DevBuf<double> d;
+  d.upload(ch, s);
+  out.resize((size_t)ch.size() * 8 * hcount(P_MAX));
+  k_rshift<<<grid_for(ch.size() * 8, 64), 64, 0, s>>>(d.get(), (int)ch.size(), out.get());
+  FMM_LAUNCH_CHECK();
+  FMM_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+void plan_make_items(const Tree& tgt, const Tree& src, const std::vector<int>& row,
+                     const std::vector<int>& srcl, int chunk, std::vector<P2PItem>& items,
+                     std::vector<int>& item_begin, int64_t& part_len, int64_t& interactions) {
+  items.clear();
+  item_begin.assign(tgt.n_leaves + 1, 0);
+  part_len = 0;
+  interactions = 0;
+  for (int li = 0; li < tgt.n_leaves; ++li) {
+    const int t = tgt.h_leaves[li];
+    const int nt = tgt.h_body_count[t];
+    item_begin[li] = (int)items.size();
+    int b = row[t];
+    const int e = row[t + 1];
+    while (b < e) {
+      int acc = 0, k = b;
+      while (k < e && (acc == 0 || acc + src.h_body_count[srcl[k]] <= chunk)) {
+        acc += src.h_body_count[srcl[k]];
+        ++k;
+      }
+      items.push_back(P2PItem{t, b, k, (int)part_len});
+      part_len += nt;
+      interactions += (int64_t)acc * nt;
+      b = k;
+    }
+  }
+  item_begin[tgt.n_leaves] = (int)items.size();
+}
+
+void plan_dense_items(const Plan& plan, std::vector<P2PItem>& items, std::vector<int>& row,
+                      std::vector<int>& srcl, std::vector<int>& item_begin, int64_t& part_len) {
+  const Tree& T = plan.tgt;
+  const Tree& S = plan.src;
+  row.assign(T.n_cells + 1, 0);
+  srcl.clear();
+  for (int c = 0; c < T.n_cells; ++c) {
+    row[c] = (int)srcl.size();
+    if (T.h_is_leaf[c])
+      for (int sl : S.h_leaves) srcl.push_back(sl);
+  }
+  row[T.n_cells] = (int)srcl.size();
+  int64_t inter = 0;
+  plan_make_items(T, S, row, srcl, 2048, items, item_begin, part_len, inter);
+}
+
+void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s) {
+  FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
+  if (plan.igrid_p >= p) return;
+  const int order = 2 * p;
+  plan.igrid.resize((size_t)std::max(plan.n_offsets, 1) * hcount(order));
+  if (plan.n_offsets)
+    k_igrid<<<grid_for(plan.n_offsets, 64), 64, 0, s>>>(plan.off_d.get(), plan.n_offsets, order,
+                                                         plan.igrid.get());
+  FMM_LAUNCH_CHECK();
+  FMM_CUDA(cudaStreamSynchronize(s));
+  plan.igrid_p = p;
+}
+
+void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt_xyz, int64_t nt,
+                int n_crit, double theta, int max_depth, cudaStream_t s) {
+  FMM_REQUIRE(ns > 0 && nt > 0, "points must be nonempty (N, 3) arrays");
+  FMM_REQUIRE(ns < (1ll << 31) && nt < (1ll << 31), "too many points");
+  FMM_REQUIRE(n_crit >= 1, "n_crit must be >= 1");
+  FMM_REQUIRE(theta > 0.0 && theta < 1.0, "theta must be in (0, 1)");
+  FMM_REQUIRE(max_depth >= 1 && max_depth <= MAX_DEPTH_LIMIT, "max_depth must be in [1, 21]");
+  plan.n_crit = n_crit;
+  plan.theta = theta;
+  plan.max_depth = max_depth;
+  build_trees(plan, src_xyz, ns, tgt_xyz, nt, s);
+
+  std::vector<int2> m2l, p2p;
+  traverse(plan, m2l, p2p, s);
+  const Tree& S = plan.src;
+  const Tree& T = plan.tgt;
+
+  // M2L CSR by target cell and the distinct-offset table.  Offsets between
+  // cell centres are exact multiples of the smaller half width (centres sit
+  // at odd multiples of their half width from the root corner), so the key
+  // (level_s, level_t, round(D / h_min)) identifies the translation; the
+  // reference groups the same pairs by D rounded to half * 2^-(max_depth+2)
+  // (fmm.py:144-159), which lands on the same lattice vectors.
+  plan.n_m2l = (int)m2l.size();
+  plan.h_m2l_row.assign(T.n_cells + 1, 0);
+  plan.h_m2l_src.resize(m2l.size());
+  std::vector<int> offid(m2l.size());
+  std::map<std::tuple<int, int, long long, long long, long long>, int> offmap;
+  std::vector<double> offd;
+  for (size_t k = 0; k < m2l.size(); ++k) {
+    const int sc = m2l[k].x, tc = m2l[k].y;
+    plan.h_m2l_row[tc + 1]++;
+    plan.h_m2l_src[k] = sc;
+    const int ls = S.h_level[sc], lt = T.h_level[tc];
+    // both trees share the root cube, so the finer cell's half width is exact
+    const double hmin = std::ldexp(plan.root_half, -std::max(ls, lt));
+    const double D[3] = {T.h_cx[tc] - S.h_cx[sc], T.h_cy[tc] - S.h_cy[sc], T.h_cz[tc] - S.h_cz[sc]};
+    long long q[3];
+    for (int d = 0; d < 3; ++d) q[d] = llround(D[d] / hmin);
+    auto key = std::make_tuple(ls, lt, q[0], q[1], q[2]);
+    auto it = offmap.find(key);
+    if (it == offmap.end()) {
+      it = offmap.emplace(key, (int)(offd.size() / 3)).first;
+      for (int d = 0; d < 3; ++d) offd.push_back((double)q[d] * hmin);
+    }
+    offid[k] = it->second;
+  }
+  for (int c = 0; c < T.n_cells; ++c) plan.h_m2l_row[c + 1] += plan.h_m2l_row[c];
+  plan.n_offsets = (int)(offd.size() / 3);
+  plan.m2l_row.upload(plan.h_m2l_row, s);
+  plan.m2l_src.upload(plan.h_m2l_src, s);
+  plan.m2l_off.upload(offid, s);
+  plan.off_d.upload(offd, s);
+  plan.m2l_tgt_cells.clear();
+  for (int c = 0; c < T.n_cells; ++c)
+    if (plan.h_m2l_row[c + 1] > plan.h_m2l_row[c]) plan.m2l_tgt_cells.push_back(c);
+  plan.d_m2l_tgt_cells.upload(plan.m2l_tgt_cells, s);
+  plan.igrid_p = -1;
+
+  // P2P CSR by target leaf and the balanced work items
+  plan.n_p2p = (int)p2p.size();
+  plan.h_p2p_row.assign(T.n_cells + 1, 0);
+  plan.h_p2p_src.resize(p2p.size());
+  for (size_t k = 0; k < p2p.size(); ++k) {
+    plan.h_p2p_row[p2p[k].y + 1]++;
+    plan.h_p2p_src[k] = p2p[k].x;
+  }
+  for (int c = 0; c < T.n_cells; ++c) plan.h_p2p_row[c + 1] += plan.h_p2p_row[c];
+  plan.p2p_row.upload(plan.h_p2p_row, s);
+  plan.p2p_src.upload(plan.h_p2p_src, s);
+  std::vector<int> item_begin;
+  plan_make_items(T, S, plan.h_p2p_row, plan.h_p2p_src, 1024, plan.items, item_begin,
+                  plan.part_len, plan.p2p_interactions);
+  plan.d_items.upload(plan.items, s);
+  plan.tleaf_item_begin.upload(item_begin, s);
+
+  build_rshift(S, plan.rshift_src, s);
+  build_rshift(T, plan.rshift_tgt, s);
+  FMM_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace fmmbem
