@@ -124,6 +124,11 @@ int fmmbem_op_gmres_device(fmmbem_op* op, const double* b_dev, double tol, int p
  * and the number of timed applies, reset them; use_graphs toggles CUDA graphs. */
 int fmmbem_op_set_timing(fmmbem_op* op, int enable, int use_graphs);
 int fmmbem_op_stage_times(fmmbem_op* op, double* ms6, int64_t* calls, int reset);
+/* cumulative kernel launches issued by the op (graph kernel nodes included), number of
+ * graph-launched applies, and the CUDA-event duration of the last fmmbem_op_gmres*
+ * call (for the host variant: H2D of b .. D2H of x inclusive). */
+int fmmbem_op_counters(fmmbem_op* op, int64_t* kernel_launches, int64_t* applies,
+                       double* last_call_ms);
 
 #ifdef __cplusplus
 }

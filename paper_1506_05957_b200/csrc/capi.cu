@@ -373,12 +373,18 @@ int fmmbem_op_gmres(fmmbem_op* h, const double* b, double tol, int p_initial, in
     FMM_REQUIRE(h && b && x, "null argument");
     select(h->device);
     BemOp& op = *h->op;
-    DevBuf<double> db, dx(op.n);
-    db.upload(b, op.n, op.s_main);
-    gmres_common(h, db.get(), tol, p_initial, p_min, relaxed, max_iter, dx.get(), residuals, orders,
-                 n_iter, converged);
-    FMM_CUDA(cudaMemcpyAsync(x, dx.get(), op.n * sizeof(double), cudaMemcpyDeviceToHost, op.s_main));
+    op.stage_x.ensure(op.n);
+    op.stage_y.ensure(op.n);
+    FMM_CUDA(cudaEventRecord(op.call_ev[0], op.s_main));
+    FMM_CUDA(cudaMemcpyAsync(op.stage_x.get(), b, op.n * sizeof(double), cudaMemcpyHostToDevice, op.s_main));
+    gmres_common(h, op.stage_x.get(), tol, p_initial, p_min, relaxed, max_iter, op.stage_y.get(),
+                 residuals, orders, n_iter, converged);
+    FMM_CUDA(cudaMemcpyAsync(x, op.stage_y.get(), op.n * sizeof(double), cudaMemcpyDeviceToHost, op.s_main));
+    FMM_CUDA(cudaEventRecord(op.call_ev[1], op.s_main));
     FMM_CUDA(cudaStreamSynchronize(op.s_main));
+    float ms = 0.f;
+    FMM_CUDA(cudaEventElapsedTime(&ms, op.call_ev[0], op.call_ev[1]));
+    op.last_call_ms = ms;
   });
 }
 
@@ -388,8 +394,15 @@ int fmmbem_op_gmres_device(fmmbem_op* h, const double* b_dev, double tol, int p_
   return guarded([&] {
     FMM_REQUIRE(h && b_dev && x_dev, "null argument");
     select(h->device);
+    BemOp& op = *h->op;
+    FMM_CUDA(cudaEventRecord(op.call_ev[0], op.s_main));
     gmres_common(h, b_dev, tol, p_initial, p_min, relaxed, max_iter, x_dev, residuals, orders,
                  n_iter, converged);
+    FMM_CUDA(cudaEventRecord(op.call_ev[1], op.s_main));
+    FMM_CUDA(cudaStreamSynchronize(op.s_main));
+    float ms = 0.f;
+    FMM_CUDA(cudaEventElapsedTime(&ms, op.call_ev[0], op.call_ev[1]));
+    op.last_call_ms = ms;
   });
 }
 
@@ -412,6 +425,16 @@ int fmmbem_op_stage_times(fmmbem_op* h, double* ms6, int64_t* calls, int reset) 
       for (auto& v : op.stage_ms) v = 0.0;
       op.stage_calls = 0;
     }
+  });
+}
+
+int fmmbem_op_counters(fmmbem_op* h, int64_t* kernel_launches, int64_t* applies,
+                       double* last_call_ms) {
+  return guarded([&] {
+    FMM_REQUIRE(h, "null argument");
+    if (kernel_launches) *kernel_launches = h->op->kernel_launches;
+    if (applies) *applies = h->op->applies;
+    if (last_call_ms) *last_call_ms = h->op->last_call_ms;
   });
 }
 

@@ -132,6 +132,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   double* nb = scal.get() + max_iter + 2;
   k_norm<<<RB, RT, 0, s>>>(n, const_cast<double*>(b), nullptr, nullptr, partials.get(), counter.get(), nb);
   FMM_LAUNCH_CHECK();
+  op.kernel_launches += 1;
   double norm_b = 0.0;
   FMM_CUDA(cudaMemcpyAsync(&norm_b, nb, sizeof(double), cudaMemcpyDeviceToHost, s));
   FMM_CUDA(cudaStreamSynchronize(s));
@@ -143,6 +144,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   }
   DevBuf<double> V((size_t)(max_iter + 1) * n);
   k_scale<<<RB, RT, 0, s>>>(n, b, nb, V.get());
+  op.kernel_launches += 1;
   std::vector<double> H((size_t)(max_iter + 1) * std::max(max_iter, 1), 0.0);
   auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * max_iter + j]; };
   std::vector<double> cs(max_iter), sn(max_iter), g(max_iter + 1, 0.0), hcol(max_iter + 2);
@@ -161,6 +163,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     k_norm<<<RB, RT, 0, s>>>(n, w, V.get() + (size_t)k * n, hd + k, partials.get(), counter.get(), hd + k + 1);
     k_normalize<<<RB, RT, 0, s>>>(n, w, hd + k + 1);
     FMM_LAUNCH_CHECK();
+    op.kernel_launches += k + 3;
     FMM_CUDA(cudaMemcpyAsync(hcol.data(), hd, (k + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaStreamSynchronize(s));
     for (int j = 0; j <= k + 1; ++j) Hat(j, k) = hcol[j];
@@ -196,6 +199,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   yd.upload(y, s);
   k_combine<<<RB, RT, 0, s>>>(n, m, V.get(), yd.get(), x);
   FMM_LAUNCH_CHECK();
+  op.kernel_launches += 1;
   FMM_CUDA(cudaStreamSynchronize(s));
   return res;
 }

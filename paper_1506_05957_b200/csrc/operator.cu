@@ -211,6 +211,7 @@ void ensure_dense(BemOp& op) {
 void clear_graphs(BemOp& op) {
   for (auto& kv : op.graphs) cudaGraphExecDestroy(kv.second);
   op.graphs.clear();
+  op.graph_kernels.clear();
 }
 
 // allocations and p-dependent tables; never called inside a stream capture.
@@ -234,7 +235,9 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
 }
 
 void record(BemOp& op, int stage, bool end, cudaStream_t s) {
-  if (op.timing) FMM_CUDA(cudaEventRecord(op.ev[2 * stage + (end ? 1 : 0)], s));
+  // External: inside a stream capture this becomes a real event-record node
+  if (op.timing)
+    FMM_CUDA(cudaEventRecordWithFlags(op.ev[2 * stage + (end ? 1 : 0)], s, cudaEventRecordExternal));
 }
 
 }  // namespace
@@ -242,6 +245,8 @@ void record(BemOp& op, int stage, bool end, cudaStream_t s) {
 BemOp::~BemOp() {
   for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
   for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : call_ev)
     if (e) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
@@ -269,6 +274,7 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_join, cudaEventDisableTiming));
   for (auto& e : op.ev) FMM_CUDA(cudaEventCreate(&e));
+  for (auto& e : op.call_ev) FMM_CUDA(cudaEventCreate(&e));
   cudaStream_t s = op.s_main;
   // collocation points are bitwise the centroid Gauss point (bemop.py:64-67)
   std::vector<double> cen(3 * P);
@@ -434,12 +440,25 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
         throw;
       }
       FMM_CUDA(cudaStreamEndCapture(s, &g));
+      size_t nn = 0;
+      FMM_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (nn) FMM_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+      int nk = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        FMM_CUDA(cudaGraphNodeGetType(nd, &ty));
+        nk += ty == cudaGraphNodeTypeKernel ? 1 : 0;
+      }
       cudaGraphExec_t ex;
       FMM_CUDA(cudaGraphInstantiate(&ex, g, 0));
       cudaGraphDestroy(g);
       it = op.graphs.emplace(key, ex).first;
+      op.graph_kernels[key] = nk;
     }
     FMM_CUDA(cudaGraphLaunch(it->second, s));
+    op.kernel_launches += op.graph_kernels[key];
+    op.applies += 1;
   } else {
     op_layer(op, c, s);
   }

@@ -59,7 +59,14 @@ struct BemOp {
 
   // CUDA graphs of apply(p), one per order
   std::map<int, cudaGraphExec_t> graphs;
+  std::map<int, int> graph_kernels;  // kernel nodes per captured graph
   std::vector<const void*> graph_sig;
+
+  // launch accounting and whole-call device timing (bench instrumentation)
+  int64_t kernel_launches = 0;
+  int64_t applies = 0;
+  cudaEvent_t call_ev[2] = {nullptr, nullptr};
+  double last_call_ms = 0.0;
   bool use_graphs = true;
 
   // stage timing

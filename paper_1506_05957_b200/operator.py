@@ -333,6 +333,15 @@ class GpuBemOperator:
     def set_timing(self, enable: bool, use_graphs: bool = True):
         N.check(self._lib.fmmbem_op_set_timing(self._h, 1 if enable else 0, 1 if use_graphs else 0))
 
+    def counters(self):
+        """(kernel launches so far, graph applies so far, last GMRES call device ms)."""
+        kl = ctypes.c_int64(0)
+        ap = ctypes.c_int64(0)
+        ms = ctypes.c_double(0.0)
+        N.check(self._lib.fmmbem_op_counters(self._h, ctypes.byref(kl), ctypes.byref(ap),
+                                             ctypes.byref(ms)))
+        return int(kl.value), int(ap.value), float(ms.value)
+
     def stage_times(self, reset: bool = False):
         """Accumulated CUDA-event ms per stage: p2p, p2m+m2m, m2l, l2l, epilogue, total."""
         ms = np.zeros(6)
