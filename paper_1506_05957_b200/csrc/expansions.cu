@@ -261,90 +261,4 @@ void launch_l2l(const TreeDev& T, const Tree& host, int p, int C, const double2*
   FMM_LAUNCH_CHECK();
 }
 
-// ------------------------------------------------------------------ M2L
-// one CTA per target cell with >= 1 interaction; sources streamed through
-// shared memory with M and I(D) expanded to full storage so the inner loop
-// is a branch-free complex dot product.
-constexpr int M2L_THREADS = 256;
-constexpr int M2L_SLOTS = 8;
-
-__global__ void __launch_bounds__(M2L_THREADS)
-k_m2l(const int* __restrict__ tcells, const int* __restrict__ row, const int* __restrict__ srcs,
-      const int* __restrict__ offs, const double2* __restrict__ igrid, int igrid_stride, int p,
-      int C, const double2* __restrict__ M, double2* __restrict__ L) {
-  extern __shared__ double2 sh[];
-  const int H = hcount(p);
-  const int S = (p + 1) * (p + 1);
-  const int Q = 2 * p;
-  double2* sM = sh;              // [C][S] full multipole
-  double2* sI = sh + C * S;      // [(2p+1)^2] full irregular grid
-  const int tc = tcells[blockIdx.x];
-  const int nout = C * H;
-  double2 acc[M2L_SLOTS];
-#pragma unroll
-  for (int s = 0; s < M2L_SLOTS; ++s) acc[s] = make_double2(0.0, 0.0);
-  for (int e = row[tc]; e < row[tc + 1]; ++e) {
-    const int sc = srcs[e];
-    const double2* Ms = M + (size_t)sc * C * H;
-    const double2* Ig = igrid + (size_t)offs[e] * igrid_stride;
-    for (int i = threadIdx.x; i < C * S; i += blockDim.x) {
-      const int c = i / S, f = i - c * S;
-      const int n = (int)sqrtf((float)f + 0.5f);
-      const int m = f - n * n - n;
-      sM[i] = hget(Ms + c * H, n, m);
-    }
-    for (int f = threadIdx.x; f < (Q + 1) * (Q + 1); f += blockDim.x) {
-      const int n = (int)sqrtf((float)f + 0.5f);
-      const int m = f - n * n - n;
-      sI[f] = hget(Ig, n, m);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int s = 0; s < M2L_SLOTS; ++s) {
-      const int t = threadIdx.x + s * M2L_THREADS;
-      if (t < nout) {
-        const int c = t / H, idx = t - c * H;
-        const int j = c_n_of[idx], k = c_m_of[idx];
-        const double2* Mc = sM + c * S;
-        double2 a = acc[s];
-        for (int n = 0; n <= p; ++n) {
-          const double2* Mrow = Mc + n * n + n;
-          const double2* Irow = sI + (n + j) * (n + j) + (n + j) + k;
-          for (int m = -n; m <= n; ++m) a = cfma_conj(Mrow[m], Irow[m], a);
-        }
-        acc[s] = a;
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int s = 0; s < M2L_SLOTS; ++s) {
-    const int t = threadIdx.x + s * M2L_THREADS;
-    if (t < nout) {
-      const int idx = t % H;
-      const double sg = (c_n_of[idx] & 1) ? -1.0 : 1.0;
-      L[(size_t)tc * nout + t] = cscale(acc[s], sg);
-    }
-  }
-}
-
-void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, cudaStream_t st) {
-  const int n = (int)plan.m2l_tgt_cells.size();
-  if (!n) return;
-  FMM_REQUIRE(C * hcount(p) <= M2L_SLOTS * M2L_THREADS, "M2L: too many outputs per cell");
-  const int S = (p + 1) * (p + 1);
-  const size_t smem = ((size_t)C * S + (2 * p + 1) * (2 * p + 1)) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    const int SM = (P_MAX + 1) * (P_MAX + 1);
-    FMM_CUDA(cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)((7 * SM + (2 * P_MAX + 1) * (2 * P_MAX + 1)) * sizeof(double2))));
-    attr = true;
-  }
-  k_m2l<<<n, M2L_THREADS, smem, st>>>(plan.d_m2l_tgt_cells.get(), plan.m2l_row.get(),
-                                      plan.m2l_src.get(), plan.m2l_off.get(), plan.igrid.get(),
-                                      hcount(2 * plan.igrid_p), p, C, M, L);
-  FMM_LAUNCH_CHECK();
-}
-
 }  // namespace fmmbem

@@ -28,7 +28,10 @@ void launch_p2m(const TreeDev& S, const int* leaves, int n_leaves, int p, int C,
                 const double* d, double2* M, cudaStream_t st);
 void launch_m2m(const TreeDev& S, const Tree& host, int p, int C, const double2* rshift,
                 double2* M, cudaStream_t st);
-void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, cudaStream_t st);
+// M2L into per-item partial blocks (part: n_items * C * hcount(p)) then reduced into L (all cells)
+void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
+                cudaStream_t st);
+void compute_igrid_full(const double* d_off, int n_off, int order, double2* out, cudaStream_t s);
 void launch_l2l(const TreeDev& T, const Tree& host, int p, int C, const double2* rshift,
                 double2* L, cudaStream_t st);
 

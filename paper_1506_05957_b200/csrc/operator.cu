@@ -230,6 +230,7 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
     op.part.ensure((size_t)std::max<int64_t>(op.plan.part_len, 1) * 3);
     op.M.ensure((size_t)op.plan.src.n_cells * C * hcount(p));
     op.L.ensure((size_t)op.plan.tgt.n_cells * C * hcount(p));
+    op.m2l_part.ensure((size_t)std::max<size_t>(op.plan.m2l_items.size(), 1) * C * hcount(p));
     plan_ensure_igrid(op.plan, p, op.s_main);
   }
 }
@@ -350,9 +351,8 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s) {
     launch_p2m(S, pl.src.leaves.get(), pl.src.n_leaves, c.p, C, q, d, op.M.get(), s);
     launch_m2m(S, pl.src, c.p, C, pl.rshift_src.get(), op.M.get(), s);
     record(op, ST_UP, true, s);
-    FMM_CUDA(cudaMemsetAsync(op.L.get(), 0, (size_t)pl.tgt.n_cells * C * hcount(c.p) * sizeof(double2), s));
     record(op, ST_M2L, false, s);
-    launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), s);
+    launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);
     record(op, ST_DOWN, false, s);
     launch_l2l(T, pl.tgt, c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
@@ -423,7 +423,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     // captured graphs bake in buffer addresses: any reallocation invalidates them
     const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
-                                          op.x_in.get(), op.y_out.get()};
+                                          op.x_in.get(), op.y_out.get(), op.m2l_part.get()};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;
@@ -521,11 +521,11 @@ void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig
   if (parts & 1) {
     plan_ensure_igrid(plan, p, s);
     DevBuf<double2> M((size_t)plan.src.n_cells * C * hcount(p)), L((size_t)plan.tgt.n_cells * C * hcount(p));
-    L.zero(s);
+    DevBuf<double2> part((size_t)std::max<size_t>(plan.m2l_items.size(), 1) * C * hcount(p));
     launch_p2m(S, plan.src.leaves.get(), plan.src.n_leaves, p, C, q_orig ? qs.get() : nullptr,
                d_orig ? ds.get() : nullptr, M.get(), s);
     launch_m2m(S, plan.src, p, C, plan.rshift_src.get(), M.get(), s);
-    launch_m2l(plan, p, C, M.get(), L.get(), s);
+    launch_m2l(plan, p, C, M.get(), L.get(), part.get(), s);
     launch_l2l(T, plan.tgt, p, C, plan.rshift_tgt.get(), L.get(), s);
     launch_l2p_channels(T, plan.tgt.leaves.get(), plan.tgt.n_leaves, p, C, want_grad, L.get(), pot,
                         grad, s);

@@ -61,8 +61,12 @@ struct Plan {
   std::vector<int> h_m2l_row, h_m2l_src;
   int n_offsets = 0;
   DevBuf<double> off_d;    // 3 * n_offsets, the (lattice-exact) translation vectors
-  DevBuf<double2> igrid;   // n_offsets * hcount(2 * igrid_p)
+  DevBuf<double2> igrid;   // n_offsets * (2 igrid_p + 1)^2, FULL flat storage n^2+n+m
   int igrid_p = -1;        // I tables hold orders up to 2 * igrid_p
+  // M2L work items: (target cell, pair begin, pair end, item id), <= 16 pairs each
+  std::vector<int4> m2l_items;
+  DevBuf<int4> d_m2l_items;
+  DevBuf<int> m2l_cell_items;  // n_tgt_cells + 1 offsets into m2l_items
   std::vector<int> m2l_tgt_cells;  // target cells with >= 1 M2L source
   DevBuf<int> d_m2l_tgt_cells;
 

@@ -15,7 +15,7 @@
 #include <map>
 #include <tuple>
 
-#include "plan.cuh"
+#include "kernels.cuh"
 
 namespace fmmbem {
 
@@ -112,13 +112,6 @@ void traverse(Plan& plan, std::vector<int2>& m2l, std::vector<int2>& p2p, cudaSt
   sort_pairs_tgt_major(p2p);
 }
 
-// I_n^m(D) for every distinct M2L offset, orders n <= 2p, half storage
-__global__ void k_igrid(const double* off, int n_off, int order, double2* out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_off) return;
-  irregular_half(off[3 * i], off[3 * i + 1], off[3 * i + 2], order, out + (size_t)i * hcount(order));
-}
-
 // R_n^m(d) for the 8 child offsets (+-h, +-h, +-h) of every level (M2M/L2L operators)
 __global__ void k_rshift(const double* child_half, int n_levels, double2* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -191,11 +184,8 @@ void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s) {
   FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
   if (plan.igrid_p >= p) return;
   const int order = 2 * p;
-  plan.igrid.resize((size_t)std::max(plan.n_offsets, 1) * hcount(order));
-  if (plan.n_offsets)
-    k_igrid<<<grid_for(plan.n_offsets, 64), 64, 0, s>>>(plan.off_d.get(), plan.n_offsets, order,
-                                                         plan.igrid.get());
-  FMM_LAUNCH_CHECK();
+  plan.igrid.resize((size_t)std::max(plan.n_offsets, 1) * (order + 1) * (order + 1));
+  compute_igrid_full(plan.off_d.get(), plan.n_offsets, order, plan.igrid.get(), s);
   FMM_CUDA(cudaStreamSynchronize(s));
   plan.igrid_p = p;
 }
@@ -258,6 +248,22 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
     if (plan.h_m2l_row[c + 1] > plan.h_m2l_row[c]) plan.m2l_tgt_cells.push_back(c);
   plan.d_m2l_tgt_cells.upload(plan.m2l_tgt_cells, s);
   plan.igrid_p = -1;
+  // M2L items: each target cell's list cut into near-equal slices of <= 16 pairs
+  plan.m2l_items.clear();
+  std::vector<int> cell_items(T.n_cells + 1, 0);
+  for (int c = 0; c < T.n_cells; ++c) {
+    cell_items[c] = (int)plan.m2l_items.size();
+    const int b = plan.h_m2l_row[c], e = plan.h_m2l_row[c + 1], len = e - b;
+    if (!len) continue;
+    const int nch = (len + 15) / 16;
+    for (int q = 0; q < nch; ++q) {
+      const int lo = b + (int)((int64_t)len * q / nch), hi = b + (int)((int64_t)len * (q + 1) / nch);
+      plan.m2l_items.push_back(make_int4(c, lo, hi, (int)plan.m2l_items.size()));
+    }
+  }
+  cell_items[T.n_cells] = (int)plan.m2l_items.size();
+  plan.d_m2l_items.upload(plan.m2l_items, s);
+  plan.m2l_cell_items.upload(cell_items, s);
 
   // P2P CSR by target leaf and the balanced work items
   plan.n_p2p = (int)p2p.size();
