@@ -258,15 +258,9 @@ def run_ours(args, cfg, mesh, world):
     stages, calls = op.stage_times(reset=True)
     dev_ms = float(np.sum(step_ms))
     applies = applies1 - applies0
-    if dist:
-        t = torch.tensor([dev_ms, float(applies)], dtype=torch.float64, device=f"cuda:{device}")
-        tmax = t.clone()
-        tdist.all_reduce(tmax, op=tdist.ReduceOp.MAX)
-        tsum = t.clone()
-        tdist.all_reduce(tsum, op=tdist.ReduceOp.SUM)
-        dev_ms_max, total_applies = float(tmax[0]), float(tsum[1])
-    else:
-        dev_ms_max, total_applies = dev_ms, float(applies)
+    from paper_1506_05957_b200.parallel import reduce_timing
+
+    dev_ms_max, total_applies = reduce_timing(dev_ms, applies, device=f"cuda:{device}")
     value = total_applies / (dev_ms_max * 1e-3)
 
     # e2e through the public API: host pinned b -> solve() -> host x

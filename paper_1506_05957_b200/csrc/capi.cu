@@ -290,6 +290,7 @@ int fmmbem_op_apply(fmmbem_op* h, const double* x, double* y, int p) {
     op_apply_device(op, op.stage_x.get(), op.stage_y.get(), p);
     FMM_CUDA(cudaMemcpyAsync(y, op.stage_y.get(), op.n * sizeof(double), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaStreamSynchronize(s));
+    op_collect_stage_times(op);
   });
 }
 
@@ -300,6 +301,7 @@ int fmmbem_op_apply_device(fmmbem_op* h, const double* x_dev, double* y_dev, int
     select(h->device);
     op_apply_device(*h->op, x_dev, y_dev, p);
     FMM_CUDA(cudaStreamSynchronize(h->op->s_main));
+    op_collect_stage_times(*h->op);
   });
 }
 

@@ -81,15 +81,28 @@ __device__ __forceinline__ double2 hget(const double2* c, int n, int m) {
 }
 
 // ------------------------------------------------ solid harmonics (harmonics.py:38-85)
+// Reciprocal table (device, read through the read-only cache) replacing the
+// fp64 divisions of the recurrences: rec[n*(P_MAX+1)+m] = 1/((n+m)(n-m)) for
+// n >= m+2, and rec[REC_DIAG+m] = -1/(2m) for m >= 1.
+constexpr int REC_DIAG = (P_MAX + 1) * (P_MAX + 1);
+constexpr int REC_SIZE = REC_DIAG + P_MAX + 1;
+inline std::vector<double> make_recip_table() {
+  std::vector<double> t(REC_SIZE, 0.0);
+  for (int n = 0; n <= P_MAX; ++n)
+    for (int m = 0; m + 2 <= n; ++m) t[n * (P_MAX + 1) + m] = 1.0 / (double)((n + m) * (n - m));
+  for (int m = 1; m <= P_MAX; ++m) t[REC_DIAG + m] = -1.0 / (2.0 * m);
+  return t;
+}
+
 // Regular R_n^m(r) = rho^n P_n^m e^{im b}/(n+m)!, m >= 0, n <= p, into out[hidx].
-__device__ inline void regular_half(double x, double y, double z, int p, double2* out) {
+__device__ inline void regular_half(double x, double y, double z, int p, double2* out,
+                                    const double* __restrict__ rec) {
   const double rho2 = x * x + y * y + z * z;
   double2 diag = make_double2(1.0, 0.0);
   for (int m = 0; m <= p; ++m) {
     if (m > 0) {
       // R_m^m = -(x + i y) / (2m) * R_{m-1}^{m-1}
-      const double s = -1.0 / (2.0 * m);
-      diag = cscale(cmul(make_double2(x, y), diag), s);
+      diag = cscale(cmul(make_double2(x, y), diag), __ldg(rec + REC_DIAG + m));
     }
     out[hidx(m, m)] = diag;
     if (m + 1 <= p) {
@@ -97,7 +110,34 @@ __device__ inline void regular_half(double x, double y, double z, int p, double2
       double2 prev1 = cscale(diag, z);
       out[hidx(m + 1, m)] = prev1;
       for (int n = m + 2; n <= p; ++n) {
-        const double inv = 1.0 / (double)((n + m) * (n - m));
+        const double inv = __ldg(rec + n * (P_MAX + 1) + m);
+        double2 cur;
+        cur.x = ((2 * n - 1) * z * prev1.x - rho2 * prev2.x) * inv;
+        cur.y = ((2 * n - 1) * z * prev1.y - rho2 * prev2.y) * inv;
+        out[hidx(n, m)] = cur;
+        prev2 = prev1;
+        prev1 = cur;
+      }
+    }
+  }
+}
+
+// Same values as regular_half, but only the columns m = m0, m0 + mstep, ...
+// (several threads cooperate on one point; the sectoral chain is cheap).
+__device__ inline void regular_half_cols(double x, double y, double z, int p, double2* out,
+                                         int m0, int mstep, const double* __restrict__ rec) {
+  const double rho2 = x * x + y * y + z * z;
+  double2 diag = make_double2(1.0, 0.0);
+  for (int m = 0; m <= p; ++m) {
+    if (m > 0) diag = cscale(cmul(make_double2(x, y), diag), __ldg(rec + REC_DIAG + m));
+    if (m < m0 || (m - m0) % mstep) continue;
+    out[hidx(m, m)] = diag;
+    if (m + 1 <= p) {
+      double2 prev2 = diag;
+      double2 prev1 = cscale(diag, z);
+      out[hidx(m + 1, m)] = prev1;
+      for (int n = m + 2; n <= p; ++n) {
+        const double inv = __ldg(rec + n * (P_MAX + 1) + m);
         double2 cur;
         cur.x = ((2 * n - 1) * z * prev1.x - rho2 * prev2.x) * inv;
         cur.y = ((2 * n - 1) * z * prev1.y - rho2 * prev2.y) * inv;

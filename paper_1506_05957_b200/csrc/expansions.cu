@@ -31,18 +31,19 @@ void upload_index_tables() {
 }
 
 // ------------------------------------------------------------------ P2M
-// one CTA per source leaf; bodies processed CHUNK at a time: the first CHUNK
-// threads evaluate R for one body each into shared memory, then every thread
-// reduces the chunk into its own coefficients.
-constexpr int P2M_THREADS = 128;
+// One CTA per source leaf; bodies processed CHUNK at a time.  Phase A: eight
+// threads per body generate R (interleaved columns m) into shared memory.
+// Phase B: thread groups each reduce a strided subset of the chunk's bodies
+// into their own coefficient (all threads busy even at low p); groups are
+// added in a fixed order at the end.
+constexpr int P2M_THREADS = 256;
 constexpr int P2M_CHUNK = 32;
-constexpr int P2M_SLOTS = (hcount(P_MAX) + P2M_THREADS - 1) / P2M_THREADS;
 
 template <int C, bool HQ, bool HD>
 __global__ void __launch_bounds__(P2M_THREADS)
 k_p2m(TreeDev S, const int* leaves, int p, const double* __restrict__ q,
       const double* __restrict__ d, double2* __restrict__ M) {
-  extern __shared__ double2 sh_r[];  // [P2M_CHUNK][H]
+  extern __shared__ double2 sh_r[];  // [P2M_CHUNK][H], later the group reduction
   __shared__ double s_q[HQ ? C : 1][P2M_CHUNK];
   __shared__ double s_d[HD ? C : 1][P2M_CHUNK][3];
   const int H = hcount(p);
@@ -50,83 +51,89 @@ k_p2m(TreeDev S, const int* leaves, int p, const double* __restrict__ q,
   const int b0 = S.body_start[leaf], nb = S.body_count[leaf];
   const double cx = S.cx[leaf], cy = S.cy[leaf], cz = S.cz[leaf];
   const int64_t ns = S.n_points;
-  double2 acc[P2M_SLOTS][C];
+  const int G = H <= P2M_THREADS ? P2M_THREADS / H : 1;  // H <= 231 < 256 always
+  const int idx = threadIdx.x % H, g = threadIdx.x / H;
+  const bool active = g < G;
+  const int n = c_n_of[idx], m = c_m_of[idx];
+  const bool has_up = n >= 1 && m + 1 <= n - 1;
+  const bool has_dn = n >= 1 && m - 1 >= -(n - 1);
+  const bool has_z = n >= 1 && m <= n - 1;
+  double2 acc[C];
 #pragma unroll
-  for (int s = 0; s < P2M_SLOTS; ++s)
-#pragma unroll
-    for (int c = 0; c < C; ++c) acc[s][c] = make_double2(0.0, 0.0);
+  for (int c = 0; c < C; ++c) acc[c] = make_double2(0.0, 0.0);
 
   for (int base = 0; base < nb; base += P2M_CHUNK) {
     const int cnt = min(P2M_CHUNK, nb - base);
-    if (threadIdx.x < cnt) {
-      const int i = b0 + base + threadIdx.x;
-      regular_half(S.px[i] - cx, S.py[i] - cy, S.pz[i] - cz, p, sh_r + threadIdx.x * H);
+    const int bl = threadIdx.x >> 3, part = threadIdx.x & 7;
+    if (bl < cnt) {
+      const int i = b0 + base + bl;
+      regular_half_cols(S.px[i] - cx, S.py[i] - cy, S.pz[i] - cz, p, sh_r + bl * H, part, 8, S.rec);
+      if (part == 0) {
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        if (HQ) s_q[c][threadIdx.x] = q[c * ns + i];
-        if (HD) {
-          s_d[c][threadIdx.x][0] = d[(c * ns + i) * 3 + 0];
-          s_d[c][threadIdx.x][1] = d[(c * ns + i) * 3 + 1];
-          s_d[c][threadIdx.x][2] = d[(c * ns + i) * 3 + 2];
+        for (int c = 0; c < C; ++c) {
+          if (HQ) s_q[c][bl] = q[c * ns + i];
+          if (HD) {
+            s_d[c][bl][0] = d[(c * ns + i) * 3 + 0];
+            s_d[c][bl][1] = d[(c * ns + i) * 3 + 1];
+            s_d[c][bl][2] = d[(c * ns + i) * 3 + 2];
+          }
         }
       }
     }
     __syncthreads();
+    if (active) {
+      for (int b = g; b < cnt; b += G) {
+        const double2* R = sh_r + b * H;
+        double2 rv, ra, rb, rz;
+        if (HQ) rv = R[idx];
+        if (HD) {
+          // gradient-shift sources R_{n-1}^{m+1}, R_{n-1}^{m-1}, R_{n-1}^m (harmonics.py:128-140)
+          ra = has_up ? R[hidx(n - 1, m + 1)] : make_double2(0.0, 0.0);
+          rb = has_dn ? hget(R, n - 1, m - 1) : make_double2(0.0, 0.0);
+          rz = has_z ? R[hidx(n - 1, m)] : make_double2(0.0, 0.0);
+        }
 #pragma unroll
-    for (int s = 0; s < P2M_SLOTS; ++s) {
-      const int idx = threadIdx.x + s * P2M_THREADS;
-      if (idx < H) {
-        const int n = c_n_of[idx], m = c_m_of[idx];
-        // gradient-shift sources R_{n-1}^{m+1}, R_{n-1}^{m-1}, R_{n-1}^m (harmonics.py:128-140)
-        const bool has_up = n >= 1 && m + 1 <= n - 1;
-        const bool has_dn = n >= 1 && m - 1 >= -(n - 1);
-        const bool has_z = n >= 1 && m <= n - 1;
-        for (int b = 0; b < cnt; ++b) {
-          const double2* R = sh_r + b * H;
-          double2 rv, ra, rb, rz;
-          if (HQ) rv = R[idx];
+        for (int c = 0; c < C; ++c) {
+          double2 a = acc[c];
+          if (HQ) {
+            const double w = s_q[c][b];
+            a.x = fma(w, rv.x, a.x);
+            a.y = fma(w, rv.y, a.y);
+          }
           if (HD) {
-            ra = has_up ? R[hidx(n - 1, m + 1)] : make_double2(0.0, 0.0);
-            rb = has_dn ? hget(R, n - 1, m - 1) : make_double2(0.0, 0.0);
-            rz = has_z ? R[hidx(n - 1, m)] : make_double2(0.0, 0.0);
+            const double dx = 0.5 * s_d[c][b][0], dy = 0.5 * s_d[c][b][1], dz = s_d[c][b][2];
+            // 1/2 (dx - i dy) R^{m+1} - 1/2 (dx + i dy) R^{m-1} + dz R^m
+            a = cfma(make_double2(dx, -dy), ra, a);
+            a = cfma(make_double2(-dx, -dy), rb, a);
+            a.x = fma(dz, rz.x, a.x);
+            a.y = fma(dz, rz.y, a.y);
           }
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            double2 a = acc[s][c];
-            if (HQ) {
-              const double w = s_q[c][b];
-              a.x = fma(w, rv.x, a.x);
-              a.y = fma(w, rv.y, a.y);
-            }
-            if (HD) {
-              const double dx = 0.5 * s_d[c][b][0], dy = 0.5 * s_d[c][b][1], dz = s_d[c][b][2];
-              // 1/2 (dx - i dy) R^{m+1} - 1/2 (dx + i dy) R^{m-1} + dz R^m
-              a = cfma(make_double2(dx, -dy), ra, a);
-              a = cfma(make_double2(-dx, -dy), rb, a);
-              a.x = fma(dz, rz.x, a.x);
-              a.y = fma(dz, rz.y, a.y);
-            }
-            acc[s][c] = a;
-          }
+          acc[c] = a;
         }
       }
     }
     __syncthreads();
   }
+  // groups -> fixed-order sum
+  if (active)
+#pragma unroll
+    for (int c = 0; c < C; ++c) sh_r[(g * C + c) * H + idx] = acc[c];
+  __syncthreads();
   double2* out = M + (size_t)leaf * C * H;
-#pragma unroll
-  for (int s = 0; s < P2M_SLOTS; ++s) {
-    const int idx = threadIdx.x + s * P2M_THREADS;
-    if (idx < H)
-#pragma unroll
-      for (int c = 0; c < C; ++c) out[c * H + idx] = acc[s][c];
+  for (int t = threadIdx.x; t < C * H; t += blockDim.x) {
+    const int c = t / H, ii = t - c * H;
+    double2 s = make_double2(0.0, 0.0);
+    for (int gg = 0; gg < G; ++gg) s = cadd(s, sh_r[(gg * C + c) * H + ii]);
+    out[c * H + ii] = s;
   }
 }
 
 template <int C, bool HQ, bool HD>
 void launch_p2m_t(const TreeDev& S, const int* leaves, int n_leaves, int p, const double* q,
                   const double* d, double2* M, cudaStream_t st) {
-  const size_t smem = (size_t)P2M_CHUNK * hcount(p) * sizeof(double2);
+  const int H = hcount(p);
+  const int G = P2M_THREADS / H;
+  const size_t smem = (size_t)std::max(P2M_CHUNK * H, G * C * H) * sizeof(double2);
   static bool attr = false;
   if (!attr) {
     FMM_CUDA(cudaFuncSetAttribute(k_p2m<C, HQ, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -154,109 +161,163 @@ void launch_p2m(const TreeDev& S, const int* leaves, int n_leaves, int p, int C,
 }
 
 // ------------------------------------------------------------------ M2M
-// one CTA per cell of `level`; internal cells gather their children.
+// One CTA per internal cell of a level.  All children's multipoles and the
+// R(d) of their octants are staged in FULL storage in shared memory, then
+// every (child, channel, coefficient) contribution is computed by its own
+// thread with branch-free index arithmetic (no per-child barriers), and the
+// children are summed in octant order.  Channels are processed in groups
+// small enough for shared memory.
 constexpr int VERT_THREADS = 256;
+constexpr int M2M_THREADS = 1024;
+constexpr size_t VERT_SMEM_BUDGET = 200 * 1024;
 
-__global__ void __launch_bounds__(VERT_THREADS)
-k_m2m(TreeDev S, int cell0, int cell1, int p, int C, const double2* __restrict__ rshift,
-      double2* __restrict__ M) {
-  extern __shared__ double2 sh[];  // [C*H] child coefficients + [H] R(d)
-  const int cell = cell0 + blockIdx.x;
-  if (cell >= cell1 || S.is_leaf[cell]) return;
-  const int H = hcount(p);
-  double2* sM = sh;
-  double2* sR = sh + C * H;
-  const int nout = C * H;
-  double2 acc[8];
-  for (int s = 0; s < 8; ++s) acc[s] = make_double2(0.0, 0.0);
-  const int fc = S.first_child[cell], nc = S.n_child[cell];
-  for (int k = 0; k < nc; ++k) {
-    const int ch = fc + k;
-    const int o = (S.cx[ch] > S.cx[cell] ? 1 : 0) | (S.cy[ch] > S.cy[cell] ? 2 : 0) |
-                  (S.cz[ch] > S.cz[cell] ? 4 : 0);
-    const double2* R = rshift + ((size_t)S.level[ch] * 8 + o) * hcount(P_MAX);
-    for (int i = threadIdx.x; i < nout; i += blockDim.x) sM[i] = M[(size_t)ch * nout + i];
-    for (int i = threadIdx.x; i < H; i += blockDim.x) sR[i] = R[i];
-    __syncthreads();
-    for (int s = 0, t = threadIdx.x; t < nout; ++s, t += blockDim.x) {
-      const int c = t / H, idx = t - c * H;
-      const int n = c_n_of[idx], m = c_m_of[idx];
-      const double2* Mc = sM + c * H;
-      double2 a = acc[s];
-      for (int j = 0; j <= n; ++j) {
-        const int kmin = max(-j, m - (n - j)), kmax = min(j, m + (n - j));
-        for (int kk = kmin; kk <= kmax; ++kk) a = cfma(hget(Mc, j, kk), hget(sR, n - j, m - kk), a);
-      }
-      acc[s] = a;
-    }
-    __syncthreads();
+__device__ __forceinline__ void expand_full(const double2* half, double2* full, int S, int tid,
+                                            int nthreads) {
+  for (int f = tid; f < S; f += nthreads) {
+    const int n = (int)sqrtf((float)f + 0.5f);
+    full[f] = hget(half, n, f - n * n - n);
   }
-  for (int s = 0, t = threadIdx.x; t < nout; ++s, t += blockDim.x) M[(size_t)cell * nout + t] = acc[s];
 }
 
-void launch_m2m(const TreeDev& S, const Tree& host, int p, int C, const double2* rshift,
-                double2* M, cudaStream_t st) {
-  const int H = hcount(p);
-  FMM_REQUIRE(C * H <= 8 * VERT_THREADS, "M2M: too many coefficients per cell");
-  const size_t smem = (size_t)(C + 1) * H * sizeof(double2);
+__global__ void __launch_bounds__(M2M_THREADS)
+k_m2m(TreeDev S, const int* __restrict__ cells, int p, int Ctot, int cbase, int Ck,
+      const double2* __restrict__ rfull, double2* __restrict__ M) {
+  extern __shared__ double2 sh[];
+  const int cell = cells[blockIdx.x];
+  const int H = hcount(p), SF = (p + 1) * (p + 1), SP = (P_MAX + 1) * (P_MAX + 1);
+  const int fc = S.first_child[cell], nc = S.n_child[cell];
+  double2* sM = sh;                 // [8][Ck][SF]
+  double2* sR = sM + 8 * Ck * SF;   // [8][SF]
+  double2* sP = sR + 8 * SF;        // [8][Ck][H]
+  for (int ci = 0; ci < nc; ++ci) {
+    const int ch = fc + ci;
+    const int o = (S.cx[ch] > S.cx[cell] ? 1 : 0) | (S.cy[ch] > S.cy[cell] ? 2 : 0) |
+                  (S.cz[ch] > S.cz[cell] ? 4 : 0);
+    const double2* R = rfull + ((size_t)S.level[ch] * 8 + o) * SP;
+    for (int f = threadIdx.x; f < SF; f += blockDim.x) sR[ci * SF + f] = R[f];
+    for (int c = 0; c < Ck; ++c)
+      expand_full(M + ((size_t)ch * Ctot + cbase + c) * H, sM + (ci * Ck + c) * SF, SF, threadIdx.x,
+                  blockDim.x);
+  }
+  __syncthreads();
+  const int nw = nc * Ck * H;
+  for (int w = threadIdx.x; w < nw; w += blockDim.x) {
+    const int ci = w / (Ck * H), r = w - ci * Ck * H, c = r / H, idx = r - c * H;
+    const int n = c_n_of[idx], m = c_m_of[idx];
+    const double2* Mc = sM + (ci * Ck + c) * SF;
+    const double2* Rc = sR + ci * SF;
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    for (int j = 0; j <= n; ++j) {
+      const int kmin = max(-j, m - (n - j)), kmax = min(j, m + (n - j));
+      const double2* Mrow = Mc + j * j + j;
+      const double2* Rrow = Rc + (n - j) * (n - j) + (n - j) + m;  // R_{n-j}^{m-k} = Rrow[-k]
+      int kk = kmin;
+      for (; kk + 1 <= kmax; kk += 2) {
+        a0 = cfma(Mrow[kk], Rrow[-kk], a0);
+        a1 = cfma(Mrow[kk + 1], Rrow[-kk - 1], a1);
+      }
+      if (kk <= kmax) a0 = cfma(Mrow[kk], Rrow[-kk], a0);
+    }
+    sP[w] = cadd(a0, a1);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < Ck * H; t += blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int ci = 0; ci < nc; ++ci) s = cadd(s, sP[ci * Ck * H + t]);
+    const int c = t / H, idx = t - c * H;
+    M[((size_t)cell * Ctot + cbase + c) * H + idx] = s;
+  }
+}
+
+static int vert_group(int p, int C, int per_ck, int fixed) {
+  // largest channel group (<= C) whose shared-memory footprint fits the budget
+  for (int ck = C; ck >= 1; --ck)
+    if ((size_t)(per_ck * ck + fixed) * sizeof(double2) <= VERT_SMEM_BUDGET) return ck;
+  throw ArgumentError("expansion order too large for the M2M/L2L shared-memory tiles");
+}
+
+void launch_m2m(const TreeDev& S, const std::vector<int>& level_off, const int* cells, int p, int C,
+                const double2* rfull, double2* M, cudaStream_t st) {
+  const int H = hcount(p), SF = (p + 1) * (p + 1);
+  const int ckmax = vert_group(p, C, 8 * SF + 8 * H, 8 * SF);
   static bool attr = false;
   if (!attr) {
     FMM_CUDA(cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(8 * hcount(P_MAX) * sizeof(double2))));
+                                  (int)VERT_SMEM_BUDGET));
     attr = true;
   }
-  for (int l = host.n_levels - 2; l >= 0; --l) {
-    const int a = host.level_start[l], b = host.level_start[l + 1];
-    if (b > a) k_m2m<<<b - a, VERT_THREADS, smem, st>>>(S, a, b, p, C, rshift, M);
+  // level_off[l]..level_off[l+1]: parents at level l whose multipole is needed; deepest first
+  for (int l = (int)level_off.size() - 2; l >= 0; --l) {
+    const int a = level_off[l], b = level_off[l + 1];
+    if (b <= a) continue;
+    for (int cb = 0; cb < C; cb += ckmax) {
+      const int ck = std::min(ckmax, C - cb);
+      const size_t smem = (size_t)(8 * ck * SF + 8 * SF + 8 * ck * H) * sizeof(double2);
+      k_m2m<<<b - a, M2M_THREADS, smem, st>>>(S, cells + a, p, C, cb, ck, rfull, M);
+    }
   }
   FMM_LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------------------ L2L
+// One CTA per cell of a level (>= 1): the parent's local expansion (full
+// storage) and R(child - parent) are staged in shared memory.
 __global__ void __launch_bounds__(VERT_THREADS)
-k_l2l(TreeDev T, int cell0, int cell1, int p, int C, const double2* __restrict__ rshift,
-      double2* __restrict__ L) {
+k_l2l(TreeDev T, const int* __restrict__ cells, int p, int Ctot, int cbase, int Ck,
+      const double2* __restrict__ rfull, double2* __restrict__ L) {
   extern __shared__ double2 sh[];
-  const int cell = cell0 + blockIdx.x;
-  if (cell >= cell1) return;
-  const int H = hcount(p);
-  const int nout = C * H;
+  const int cell = cells[blockIdx.x];
+  const int H = hcount(p), SF = (p + 1) * (p + 1), SP = (P_MAX + 1) * (P_MAX + 1);
   const int par = T.parent[cell];
   const int o = (T.cx[cell] > T.cx[par] ? 1 : 0) | (T.cy[cell] > T.cy[par] ? 2 : 0) |
                 (T.cz[cell] > T.cz[par] ? 4 : 0);
-  const double2* R = rshift + ((size_t)T.level[cell] * 8 + o) * hcount(P_MAX);
-  double2* sL = sh;
-  double2* sR = sh + nout;
-  for (int i = threadIdx.x; i < nout; i += blockDim.x) sL[i] = L[(size_t)par * nout + i];
-  for (int i = threadIdx.x; i < H; i += blockDim.x) sR[i] = R[i];
+  const double2* R = rfull + ((size_t)T.level[cell] * 8 + o) * SP;
+  double2* sL = sh;             // [Ck][SF]
+  double2* sR = sL + Ck * SF;   // [SF]
+  for (int f = threadIdx.x; f < SF; f += blockDim.x) sR[f] = R[f];
+  for (int c = 0; c < Ck; ++c)
+    expand_full(L + ((size_t)par * Ctot + cbase + c) * H, sL + c * SF, SF, threadIdx.x, blockDim.x);
   __syncthreads();
-  for (int t = threadIdx.x; t < nout; t += blockDim.x) {
+  for (int t = threadIdx.x; t < Ck * H; t += blockDim.x) {
     const int c = t / H, idx = t - c * H;
     const int n = c_n_of[idx], m = c_m_of[idx];
-    const double2* Lc = sL + c * H;
-    double2 a = make_double2(0.0, 0.0);
+    const double2* Lc = sL + c * SF;
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
     for (int j = n; j <= p; ++j) {
       const int kmin = max(-j, m - (j - n)), kmax = min(j, m + (j - n));
-      for (int kk = kmin; kk <= kmax; ++kk) a = cfma(hget(Lc, j, kk), hget(sR, j - n, kk - m), a);
+      const double2* Lrow = Lc + j * j + j;
+      const double2* Rrow = sR + (j - n) * (j - n) + (j - n) - m;  // R_{j-n}^{k-m} = Rrow[k]
+      int kk = kmin;
+      for (; kk + 1 <= kmax; kk += 2) {
+        a0 = cfma(Lrow[kk], Rrow[kk], a0);
+        a1 = cfma(Lrow[kk + 1], Rrow[kk + 1], a1);
+      }
+      if (kk <= kmax) a0 = cfma(Lrow[kk], Rrow[kk], a0);
     }
-    double2 v = L[(size_t)cell * nout + t];
-    L[(size_t)cell * nout + t] = cadd(v, a);
+    double2* dst = L + ((size_t)cell * Ctot + cbase + c) * H + idx;
+    *dst = cadd(*dst, cadd(a0, a1));
   }
 }
 
-void launch_l2l(const TreeDev& T, const Tree& host, int p, int C, const double2* rshift,
-                double2* L, cudaStream_t st) {
-  const int H = hcount(p);
-  const size_t smem = (size_t)(C + 1) * H * sizeof(double2);
+void launch_l2l(const TreeDev& T, const std::vector<int>& level_off, const int* cells, int p, int C,
+                const double2* rfull, double2* L, cudaStream_t st) {
+  const int SF = (p + 1) * (p + 1);
+  const int ckmax = vert_group(p, C, SF, SF);
   static bool attr = false;
   if (!attr) {
     FMM_CUDA(cudaFuncSetAttribute(k_l2l, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(8 * hcount(P_MAX) * sizeof(double2))));
+                                  (int)VERT_SMEM_BUDGET));
     attr = true;
   }
-  for (int l = 1; l < host.n_levels; ++l) {
-    const int a = host.level_start[l], b = host.level_start[l + 1];
-    if (b > a) k_l2l<<<b - a, VERT_THREADS, smem, st>>>(T, a, b, p, C, rshift, L);
+  // level_off[l]..level_off[l+1]: cells at level l whose parent carries a local expansion
+  for (int l = 1; l + 1 < (int)level_off.size(); ++l) {
+    const int a = level_off[l], b = level_off[l + 1];
+    if (b <= a) continue;
+    for (int cb = 0; cb < C; cb += ckmax) {
+      const int ck = std::min(ckmax, C - cb);
+      const size_t smem = (size_t)(ck * SF + SF) * sizeof(double2);
+      k_l2l<<<b - a, VERT_THREADS, smem, st>>>(T, cells + a, p, C, cb, ck, rfull, L);
+    }
   }
   FMM_LAUNCH_CHECK();
 }

@@ -30,8 +30,10 @@ __device__ double block_sum(double v, double* sh) {
   return t;
 }
 
-// finish: the last block to arrive adds the block partials in block order
-__device__ void finish(double part, double* partials, unsigned* counter, double* out, bool do_sqrt) {
+// finish: the last block to arrive adds the block partials (fixed assignment
+// of partials to threads and a fixed reduction tree: deterministic)
+__device__ void finish(double part, double* partials, unsigned* counter, double* out, bool do_sqrt,
+                       double* sh) {
   __shared__ bool last;
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = part;
@@ -39,10 +41,12 @@ __device__ void finish(double part, double* partials, unsigned* counter, double*
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double t = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) t += ((volatile double*)partials)[b];
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) t += __ldcg(partials + b);
+  t = block_sum(t, sh);
+  if (threadIdx.x == 0) {
     *out = do_sqrt ? sqrt(t) : t;
     *counter = 0u;
   }
@@ -63,7 +67,7 @@ __global__ void __launch_bounds__(RT) k_mgs(int64_t n, const double* __restrict_
     }
     acc = fma(v[i], wi, acc);
   }
-  finish(block_sum(acc, sh), partials, counter, out, false);
+  finish(block_sum(acc, sh), partials, counter, out, false, sh);
 }
 
 // w -= h * v; out = ||w||    (solver.py:102-103)
@@ -81,7 +85,7 @@ __global__ void __launch_bounds__(RT) k_norm(int64_t n, double* w, const double*
     }
     acc = fma(wi, wi, acc);
   }
-  finish(block_sum(acc, sh), partials, counter, out, true);
+  finish(block_sum(acc, sh), partials, counter, out, true, sh);
 }
 
 // v = w / h (or zeros on breakdown)    (solver.py:104-107)
@@ -125,9 +129,16 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   GmresResult res;
   const int64_t n = op.n;
   cudaStream_t s = op.s_main;
-  DevBuf<double> partials(RB), scal(max_iter + 3);
-  DevBuf<unsigned> counter(1);
-  counter.zero(s);
+  // workspaces live in the operator (grow-only): no allocation inside a solve
+  DevBuf<double>& partials = op.g_partials;
+  DevBuf<double>& scal = op.g_scal;
+  DevBuf<unsigned>& counter = op.g_counter;
+  partials.ensure(RB);
+  scal.ensure(max_iter + 3);
+  if (!counter.size()) {
+    counter.ensure(1);
+    counter.zero(s);
+  }
   // ||b||
   double* nb = scal.get() + max_iter + 2;
   k_norm<<<RB, RT, 0, s>>>(n, const_cast<double*>(b), nullptr, nullptr, partials.get(), counter.get(), nb);
@@ -142,7 +153,8 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     res.converged = true;
     return res;
   }
-  DevBuf<double> V((size_t)(max_iter + 1) * n);
+  DevBuf<double>& V = op.g_basis;
+  V.ensure((size_t)(max_iter + 1) * n);
   k_scale<<<RB, RT, 0, s>>>(n, b, nb, V.get());
   op.kernel_launches += 1;
   std::vector<double> H((size_t)(max_iter + 1) * std::max(max_iter, 1), 0.0);
@@ -166,6 +178,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     op.kernel_launches += k + 3;
     FMM_CUDA(cudaMemcpyAsync(hcol.data(), hd, (k + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaStreamSynchronize(s));
+    op_collect_stage_times(op);
     for (int j = 0; j <= k + 1; ++j) Hat(j, k) = hcol[j];
     for (int j = 0; j < k; ++j) {
       const double h1 = cs[j] * Hat(j, k) + sn[j] * Hat(j + 1, k);
@@ -195,8 +208,9 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     for (int j = i + 1; j < m; ++j) t -= Hat(i, j) * y[j];
     y[i] = t / Hat(i, i);
   }
-  DevBuf<double> yd;
-  yd.upload(y, s);
+  DevBuf<double>& yd = op.g_y;
+  yd.ensure(y.size());
+  FMM_CUDA(cudaMemcpyAsync(yd.get(), y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   k_combine<<<RB, RT, 0, s>>>(n, m, V.get(), yd.get(), x);
   FMM_LAUNCH_CHECK();
   op.kernel_launches += 1;

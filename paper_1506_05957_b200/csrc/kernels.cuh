@@ -12,13 +12,14 @@ struct TreeDev {
   const int *level, *parent, *first_child, *n_child, *body_start, *body_count, *perm;
   const uint8_t* is_leaf;
   int64_t n_points;
+  const double* rec;
 };
 
 inline TreeDev tree_dev(const Tree& t) {
   return TreeDev{t.px.get(), t.py.get(), t.pz.get(), t.cx.get(), t.cy.get(), t.cz.get(),
                  t.half.get(), t.level.get(), t.parent.get(), t.first_child.get(),
                  t.n_child.get(), t.body_start.get(), t.body_count.get(), t.perm.get(),
-                 t.is_leaf.get(), t.n_points};
+                 t.is_leaf.get(), t.n_points, t.rec};
 }
 
 void upload_index_tables();
@@ -26,14 +27,16 @@ void upload_index_tables();
 // far field
 void launch_p2m(const TreeDev& S, const int* leaves, int n_leaves, int p, int C, const double* q,
                 const double* d, double2* M, cudaStream_t st);
-void launch_m2m(const TreeDev& S, const Tree& host, int p, int C, const double2* rshift,
-                double2* M, cudaStream_t st);
+// M2M over the parents listed per level (cells[level_off[l] .. level_off[l+1]])
+void launch_m2m(const TreeDev& S, const std::vector<int>& level_off, const int* cells, int p, int C,
+                const double2* rfull, double2* M, cudaStream_t st);
 // M2L into per-item partial blocks (part: n_items * C * hcount(p)) then reduced into L (all cells)
 void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
                 cudaStream_t st);
 void compute_igrid_full(const double* d_off, int n_off, int order, double2* out, cudaStream_t s);
-void launch_l2l(const TreeDev& T, const Tree& host, int p, int C, const double2* rshift,
-                double2* L, cudaStream_t st);
+// L2L into the cells listed per level whose parent has a nonzero local expansion
+void launch_l2l(const TreeDev& T, const std::vector<int>& level_off, const int* cells, int p, int C,
+                const double2* rfull, double2* L, cudaStream_t st);
 
 // near field (P2P) kinds
 enum class P2PKind : int { LAP_Q = 0, LAP_D = 1, STOKESLET = 2, STRESSLET = 3 };

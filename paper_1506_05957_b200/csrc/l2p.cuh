@@ -15,14 +15,15 @@ namespace fmmbem {
 
 template <int C, bool GRAD>
 __device__ __forceinline__ void l2p_eval(const double2* __restrict__ L, int H, int p, double x,
-                                         double y, double z, double* pot, double* grad) {
+                                         double y, double z, double* pot, double* grad,
+                                         const double* __restrict__ rec) {
   const double rho2 = x * x + y * y + z * z;
   double zr[C], zi[C], gz[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) { zr[c] = 0.0; zi[c] = 0.0; gz[c] = 0.0; }
   double2 diag = make_double2(1.0, 0.0);
   for (int m = 0; m <= p; ++m) {
-    if (m > 0) diag = cscale(cmul(make_double2(x, y), diag), -1.0 / (2.0 * m));
+    if (m > 0) diag = cscale(cmul(make_double2(x, y), diag), __ldg(rec + REC_DIAG + m));
     double2 prev2 = make_double2(0.0, 0.0), cur = diag;
     const double w = m == 0 ? 1.0 : 2.0;
     for (int n = m; n <= p; ++n) {
@@ -30,7 +31,7 @@ __device__ __forceinline__ void l2p_eval(const double2* __restrict__ L, int H, i
         prev2 = cur;
         cur = cscale(cur, z);
       } else if (n > m + 1) {
-        const double inv = 1.0 / (double)((n + m) * (n - m));
+        const double inv = __ldg(rec + n * (P_MAX + 1) + m);
         double2 nx;
         nx.x = ((2 * n - 1) * z * cur.x - rho2 * prev2.x) * inv;
         nx.y = ((2 * n - 1) * z * cur.y - rho2 * prev2.y) * inv;

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(128) k_epilogue(TreeDev T, EpiArgs a) {
     double pot[C], grad[3 * C];
 #pragma unroll
     for (int c = 0; c < C; ++c) { pot[c] = 0.0; grad[3 * c] = grad[3 * c + 1] = grad[3 * c + 2] = 0.0; }
-    if (FAR) l2p_eval<C, Tr::GRAD>(sL, H, a.p, tx - cx, ty - cy, tz - cz, pot, grad);
+    if (FAR) l2p_eval<C, Tr::GRAD>(sL, H, a.p, tx - cx, ty - cy, tz - cz, pot, grad, T.rec);
     if (KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) {
       double corr = 0.0;
       for (int e = a.rowptr[pn]; e < a.rowptr[pn + 1]; ++e) corr = fma(a.vals[e], a.x[a.cols[e]], corr);
@@ -232,6 +232,7 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
     op.L.ensure((size_t)op.plan.tgt.n_cells * C * hcount(p));
     op.m2l_part.ensure((size_t)std::max<size_t>(op.plan.m2l_items.size(), 1) * C * hcount(p));
     plan_ensure_igrid(op.plan, p, op.s_main);
+    if (kind == op.basis_kind_for_sys) op.use_basis = ensure_p2m_basis(op, p, op.s_main);
   }
 }
 
@@ -309,6 +310,7 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   if (formulation == LAPLACE_FIRST) { sys_kind = K_LAP_SINGLE; rhs_kind = K_LAP_DOUBLE; }
   else if (formulation == LAPLACE_SECOND) { sys_kind = K_LAP_DOUBLE; rhs_kind = K_LAP_SINGLE; }
   else { sys_kind = K_STOKESLET; rhs_kind = K_STRESSLET; }
+  op.basis_kind_for_sys = sys_kind;
   build_correction(op, sys_kind, op.c_sys, s);
   build_correction(op, rhs_kind, op.c_rhs, s);
   op.x_in.resize(op.n);
@@ -348,14 +350,17 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s) {
     const double* q = (c.kind == K_LAP_SINGLE || c.kind == K_STOKESLET) ? op.q.get() : nullptr;
     const double* d = (c.kind == K_LAP_DOUBLE || c.kind == K_STRESSLET) ? op.dip.get() : nullptr;
     record(op, ST_UP, false, s);
-    launch_p2m(S, pl.src.leaves.get(), pl.src.n_leaves, c.p, C, q, d, op.M.get(), s);
-    launch_m2m(S, pl.src, c.p, C, pl.rshift_src.get(), op.M.get(), s);
+    if (c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p)
+      launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s);
+    else
+      launch_p2m(S, pl.src.leaves.get(), pl.src.n_leaves, c.p, C, q, d, op.M.get(), s);
+    launch_m2m(S, pl.m2m_level_off, pl.m2m_cells.get(), c.p, C, pl.rshift_src.get(), op.M.get(), s);
     record(op, ST_UP, true, s);
     record(op, ST_M2L, false, s);
     launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);
     record(op, ST_DOWN, false, s);
-    launch_l2l(T, pl.tgt, c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
+    launch_l2l(T, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
     record(op, ST_DOWN, true, s);
   }
   FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
@@ -399,7 +404,6 @@ void sys_call(BemOp& op, int p, bool dense, const double* x, double* y, LayerCal
 
 void accumulate_stage_times(BemOp& op) {
   if (!op.timing) return;
-  FMM_CUDA(cudaStreamSynchronize(op.s_main));
   for (int st = 0; st < N_STAGES; ++st) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, op.ev[2 * st], op.ev[2 * st + 1]) == cudaSuccess)
@@ -423,7 +427,8 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     // captured graphs bake in buffer addresses: any reallocation invalidates them
     const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
-                                          op.x_in.get(), op.y_out.get(), op.m2l_part.get()};
+                                          op.x_in.get(), op.y_out.get(), op.m2l_part.get(),
+                                          op.p2m_basis.get()};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;
@@ -463,8 +468,10 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     op_layer(op, c, s);
   }
   FMM_CUDA(cudaMemcpyAsync(y, op.y_out.get(), op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  accumulate_stage_times(op);
 }
+
+// stage timers of the last apply; call only after the op's stream has been synchronised
+void op_collect_stage_times(BemOp& op) { accumulate_stage_times(op); }
 
 void op_dense_apply_device(BemOp& op, const double* x, double* y) {
   LayerCall c;
@@ -524,9 +531,9 @@ void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig
     DevBuf<double2> part((size_t)std::max<size_t>(plan.m2l_items.size(), 1) * C * hcount(p));
     launch_p2m(S, plan.src.leaves.get(), plan.src.n_leaves, p, C, q_orig ? qs.get() : nullptr,
                d_orig ? ds.get() : nullptr, M.get(), s);
-    launch_m2m(S, plan.src, p, C, plan.rshift_src.get(), M.get(), s);
+    launch_m2m(S, plan.m2m_level_off, plan.m2m_cells.get(), p, C, plan.rshift_src.get(), M.get(), s);
     launch_m2l(plan, p, C, M.get(), L.get(), part.get(), s);
-    launch_l2l(T, plan.tgt, p, C, plan.rshift_tgt.get(), L.get(), s);
+    launch_l2l(T, plan.l2l_level_off, plan.l2l_cells.get(), p, C, plan.rshift_tgt.get(), L.get(), s);
     launch_l2p_channels(T, plan.tgt.leaves.get(), plan.tgt.n_leaves, p, C, want_grad, L.get(), pot,
                         grad, s);
     FMM_CUDA(cudaStreamSynchronize(s));

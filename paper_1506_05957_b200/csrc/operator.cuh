@@ -57,6 +57,16 @@ struct BemOp {
   int64_t dense_part_len = 0;
   int dense_max_sources = 0;
 
+  // precomputed P2M basis of the system kernel ([hidx][sorted source], p2m_basis.cu)
+  int basis_kind_for_sys = -1;
+  int basis_p = -1;
+  bool use_basis = false;
+  DevBuf<double2> p2m_basis;
+
+  // GMRES workspaces (Krylov basis, reductions), grow-only
+  DevBuf<double> g_basis, g_partials, g_scal, g_y;
+  DevBuf<unsigned> g_counter;
+
   // CUDA graphs of apply(p), one per order
   std::map<int, cudaGraphExec_t> graphs;
   std::map<int, int> graph_kernels;  // kernel nodes per captured graph
@@ -94,10 +104,13 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t n_panels, const do
              int n_gauss_singular, int formulation, double theta, int n_crit, double mu,
              double near_factor, int max_depth);
 void op_layer(BemOp& op, const LayerCall& call, cudaStream_t s);
-void op_apply_device(BemOp& op, const double* x, double* y, int p);
+void op_apply_device(BemOp& op, const double* x, double* y, int p);  // async on op.s_main
+void op_collect_stage_times(BemOp& op);  // after a sync of op.s_main
 void op_dense_apply_device(BemOp& op, const double* x, double* y);
 void op_rhs_device(BemOp& op, const double* data, double* b, int p, bool dense);
 void build_near_pairs(BemOp& op, cudaStream_t s);
+bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s);  // false: over the memory budget
+void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cudaStream_t s);
 void build_correction(BemOp& op, int kind, Correction& out, cudaStream_t s);
 
 struct GmresResult {

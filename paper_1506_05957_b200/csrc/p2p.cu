@@ -30,11 +30,22 @@ template <> struct P2PTraits<P2PKind::LAP_D> { static constexpr int NW = 3, NC =
 template <> struct P2PTraits<P2PKind::STOKESLET> { static constexpr int NW = 3, NC = 3; };
 template <> struct P2PTraits<P2PKind::STRESSLET> { static constexpr int NW = 6, NC = 3; };
 
+// 1/sqrt(x) for x > 0 to ~1 ulp: the SFU's double-precision seed (MUFU.RSQ64H,
+// ~2^-22) plus one third-order Newton step, y (1 + e/2 + 3e^2/8), e = 1 - x y^2:
+// 5 DP instructions and no slow-path branch (the libdevice rsqrt carries one).
+// x == 0 yields inf/NaN and is masked by the caller (the reference's d2 > 0 rule).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x * y, y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
+}
+
 template <P2PKind K>
 __device__ __forceinline__ void interact(double rx, double ry, double rz, const double* wv,
                                          double* acc) {
   const double d2 = fma(rx, rx, fma(ry, ry, rz * rz));
-  const double inv = d2 > 0.0 ? rsqrt(d2) : 0.0;
+  const double inv = d2 > 0.0 ? rsqrt_nr(d2) : 0.0;
   if (K == P2PKind::LAP_Q) {
     acc[0] = fma(wv[0], inv, acc[0]);
   } else if (K == P2PKind::LAP_D) {
@@ -59,97 +70,99 @@ __device__ __forceinline__ void interact(double rx, double ry, double rz, const 
   }
 }
 
+// sources staged as double2 planes: (x, y), (z, w0), (w1, w2), (w3, w4), (w5, -)
+template <int NW> struct SrcPlanes { static constexpr int N = (3 + NW + 1) / 2; };
+
 template <P2PKind K>
 __global__ void __launch_bounds__(P2P_THREADS)
 k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __restrict__ p2p_src,
       int max_src, const double* __restrict__ w, double* __restrict__ part) {
   constexpr int NW = P2PTraits<K>::NW, NC = P2PTraits<K>::NC;
-  extern __shared__ double sh[];
-  double* sx = sh;
-  double* sy = sx + max_src;
-  double* sz = sy + max_src;
-  double* sw = sz + max_src;  // [NW][max_src]
+  constexpr int NPL = SrcPlanes<NW>::N;
+  constexpr int TPT = 2;  // targets per thread: every staged source is used twice
+  extern __shared__ double2 sh2[];
   const P2PItem it = items[blockIdx.x];
   int ns = 0;
   for (int k = it.pair_begin; k < it.pair_end; ++k) {
     const int leaf = p2p_src[k];
     const int s0 = S.body_start[leaf], cnt = S.body_count[leaf];
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      sx[ns + i] = S.px[s0 + i];
-      sy[ns + i] = S.py[s0 + i];
-      sz[ns + i] = S.pz[s0 + i];
+      double v[2 * NPL];
+      v[0] = S.px[s0 + i];
+      v[1] = S.py[s0 + i];
+      v[2] = S.pz[s0 + i];
 #pragma unroll
-      for (int j = 0; j < NW; ++j) sw[j * max_src + ns + i] = w[(size_t)(s0 + i) * NW + j];
+      for (int q = 0; q < NW; ++q) v[3 + q] = w[(size_t)(s0 + i) * NW + q];
+#pragma unroll
+      for (int q = 3 + NW; q < 2 * NPL; ++q) v[q] = 0.0;
+#pragma unroll
+      for (int pl = 0; pl < NPL; ++pl) sh2[pl * max_src + ns + i] = make_double2(v[2 * pl], v[2 * pl + 1]);
     }
     ns += cnt;
   }
   __syncthreads();
   const int t0 = T.body_start[it.tgt_leaf], nt = T.body_count[it.tgt_leaf];
-  const int G = nt <= (int)blockDim.x ? (int)blockDim.x / nt : 1;
-  const int g = threadIdx.x / nt;  // valid only when nt <= blockDim
-  double res[NC];
-  if (nt <= (int)blockDim.x) {
-    const int lt = threadIdx.x % nt;
-    double acc[NC];
+  const int nslot = (nt + TPT - 1) / TPT;
+  for (int sbase = 0; sbase < nslot; sbase += blockDim.x) {
+    const int nsl = min(nslot - sbase, (int)blockDim.x);
+    const int G = blockDim.x / nsl;
+    const int sl = threadIdx.x % nsl, g = threadIdx.x / nsl;
+    double acc[TPT][NC];
+    double tx[TPT], ty[TPT], tz[TPT];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    for (int q = 0; q < TPT; ++q) {
+      const int lt = min(sbase + sl + q * nslot, nt - 1);
+      tx[q] = T.px[t0 + lt];
+      ty[q] = T.py[t0 + lt];
+      tz[q] = T.pz[t0 + lt];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[q][c] = 0.0;
+    }
     if (g < G) {
-      const double tx = T.px[t0 + lt], ty = T.py[t0 + lt], tz = T.pz[t0 + lt];
-      int j = g;
-      for (; j + G < ns; j += 2 * G) {
-        double w0[NW], w1[NW];
+      for (int j = g; j < ns; j += G) {
+        double v[2 * NPL];
 #pragma unroll
-        for (int q = 0; q < NW; ++q) { w0[q] = sw[q * max_src + j]; w1[q] = sw[q * max_src + j + G]; }
-        interact<K>(tx - sx[j], ty - sy[j], tz - sz[j], w0, acc);
-        interact<K>(tx - sx[j + G], ty - sy[j + G], tz - sz[j + G], w1, acc);
-      }
-      if (j < ns) {
-        double w0[NW];
+        for (int pl = 0; pl < NPL; ++pl) {
+          const double2 u = sh2[pl * max_src + j];
+          v[2 * pl] = u.x;
+          v[2 * pl + 1] = u.y;
+        }
 #pragma unroll
-        for (int q = 0; q < NW; ++q) w0[q] = sw[q * max_src + j];
-        interact<K>(tx - sx[j], ty - sy[j], tz - sz[j], w0, acc);
+        for (int q = 0; q < TPT; ++q) interact<K>(tx[q] - v[0], ty[q] - v[1], tz[q] - v[2], v + 3, acc[q]);
       }
     }
+    __syncthreads();  // the source tile is no longer read: reuse it for the group reduction
+    double* red = reinterpret_cast<double*>(sh2);
+    if (g < G)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) res[c] = acc[c];
-    if (G > 1) {
-      __syncthreads();  // source tile no longer needed: reuse shared memory
-      if (g < G)
+      for (int q = 0; q < TPT; ++q)
 #pragma unroll
-        for (int c = 0; c < NC; ++c) sh[(g * nt + lt) * NC + c] = acc[c];
-      __syncthreads();
-      if (g == 0) {
-        for (int gg = 1; gg < G; ++gg)
+        for (int c = 0; c < NC; ++c) red[((g * TPT + q) * nsl + sl) * NC + c] = acc[q][c];
+    __syncthreads();
+    if (g == 0) {
 #pragma unroll
-          for (int c = 0; c < NC; ++c) res[c] += sh[(gg * nt + lt) * NC + c];
+      for (int q = 0; q < TPT; ++q) {
+        const int lt = sbase + sl + q * nslot;
+        if (lt >= nt) continue;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          double r = 0.0;
+          for (int gg = 0; gg < G; ++gg) r += red[((gg * TPT + q) * nsl + sl) * NC + c];
+          part[(size_t)(it.out_off + lt) * NC + c] = r;
+        }
       }
     }
-    if (g == 0)
-#pragma unroll
-      for (int c = 0; c < NC; ++c) part[(size_t)(it.out_off + lt) * NC + c] = res[c];
-  } else {
-    for (int lt = threadIdx.x; lt < nt; lt += blockDim.x) {
-      double acc[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-      const double tx = T.px[t0 + lt], ty = T.py[t0 + lt], tz = T.pz[t0 + lt];
-      for (int j = 0; j < ns; ++j) {
-        double w0[NW];
-#pragma unroll
-        for (int q = 0; q < NW; ++q) w0[q] = sw[q * max_src + j];
-        interact<K>(tx - sx[j], ty - sy[j], tz - sz[j], w0, acc);
-      }
-#pragma unroll
-      for (int c = 0; c < NC; ++c) part[(size_t)(it.out_off + lt) * NC + c] = acc[c];
-    }
+    __syncthreads();
   }
 }
 
 template <P2PKind K>
 void launch_p2p_t(const TreeDev& S, const TreeDev& T, const P2PItem* items, int n_items,
                   const int* p2p_src, int max_src, const double* w, double* part, cudaStream_t st) {
-  constexpr int NW = P2PTraits<K>::NW;
-  const size_t smem = (size_t)max_src * (3 + NW) * sizeof(double);
+  constexpr int NPL = SrcPlanes<P2PTraits<K>::NW>::N;
+  // shared memory: the staged sources, or the group reduction (256 * 2 targets * 3 comps)
+  const size_t smem = std::max((size_t)max_src * NPL * sizeof(double2),
+                               (size_t)P2P_THREADS * 2 * 3 * sizeof(double));
   FMM_REQUIRE(smem <= 227 * 1024, "P2P: source slice too large for shared memory");
   FMM_CUDA(cudaFuncSetAttribute(k_p2p<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (n_items) k_p2p<K><<<n_items, P2P_THREADS, smem, st>>>(S, T, items, p2p_src, max_src, w, part);
@@ -159,8 +172,7 @@ void launch_p2p_t(const TreeDev& S, const TreeDev& T, const P2PItem* items, int 
 void launch_p2p(P2PKind kind, const TreeDev& S, const TreeDev& T, const P2PItem* items,
                 int n_items, const int* p2p_src, int max_sources, const double* w, double* part,
                 cudaStream_t st) {
-  // shared memory must also hold the group reduction (256 * 3 doubles)
-  const int ms = std::max(max_sources, 256);
+  const int ms = std::max(max_sources, 1);
   switch (kind) {
     case P2PKind::LAP_Q: return launch_p2p_t<P2PKind::LAP_Q>(S, T, items, n_items, p2p_src, ms, w, part, st);
     case P2PKind::LAP_D: return launch_p2p_t<P2PKind::LAP_D>(S, T, items, n_items, p2p_src, ms, w, part, st);
@@ -274,7 +286,7 @@ __global__ void k_l2p_channels(TreeDev T, const int* leaves, int p, const double
     double ph[C], gr[3 * C];
 #pragma unroll
     for (int c = 0; c < C; ++c) { ph[c] = 0; gr[3 * c] = gr[3 * c + 1] = gr[3 * c + 2] = 0; }
-    l2p_eval<C, GRAD>(sL, H, p, T.px[ti] - cx, T.py[ti] - cy, T.pz[ti] - cz, ph, gr);
+    l2p_eval<C, GRAD>(sL, H, p, T.px[ti] - cx, T.py[ti] - cy, T.pz[ti] - cz, ph, gr, T.rec);
     const int o = T.perm[ti];
 #pragma unroll
     for (int c = 0; c < C; ++c) {

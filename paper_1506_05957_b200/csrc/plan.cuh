@@ -35,6 +35,7 @@ struct Tree {
   std::vector<uint8_t> h_is_leaf;
   std::vector<int> h_leaves;
   std::vector<double> h_cx, h_cy, h_cz;
+  const double* rec = nullptr;  // plan's reciprocal table (common.cuh)
 };
 
 struct P2PItem {
@@ -52,6 +53,7 @@ struct Plan {
   double root_c[3] = {0, 0, 0};
   double root_half = 0;
   Tree src, tgt;
+  DevBuf<double> recip;  // make_recip_table() on device
 
   // M2L: CSR by target cell over (source cell, offset id)
   int n_m2l = 0;
@@ -81,8 +83,13 @@ struct Plan {
   int64_t part_len = 0;          // total targets over items
   int64_t p2p_interactions = 0;
 
+  // pruned vertical passes: M2M only for parents whose multipole is needed by an
+  // M2L (or an ancestor's), L2L only below cells that carry a local expansion
+  std::vector<int> m2m_level_off, l2l_level_off;
+  DevBuf<int> m2m_cells, l2l_cells;
+
   // M2M / L2L translation tables: R(d) for the 8 child octants of every level, up to igrid... P_MAX
-  DevBuf<double2> rshift_src;  // [level][octant][hcount(P_MAX)]
+  DevBuf<double2> rshift_src;  // [level][octant][(P_MAX+1)^2] full storage
   DevBuf<double2> rshift_tgt;
 };
 

@@ -112,14 +112,20 @@ void traverse(Plan& plan, std::vector<int2>& m2l, std::vector<int2>& p2p, cudaSt
   sort_pairs_tgt_major(p2p);
 }
 
-// R_n^m(d) for the 8 child offsets (+-h, +-h, +-h) of every level (M2M/L2L operators)
-__global__ void k_rshift(const double* child_half, int n_levels, double2* out) {
+// R_n^m(d) in FULL storage for the 8 child offsets (+-h, +-h, +-h) of every
+// level (the M2M / L2L operators; fmm.py:268-290 uses the first cell's offset
+// of each octant group, here the exact lattice offset)
+__global__ void k_rshift(const double* child_half, int n_levels, double2* out,
+                         const double* rec) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_levels * 8) return;
   const int l = i / 8, o = i % 8;
   const double h = child_half[l];
-  regular_half((o & 1) ? h : -h, (o & 2) ? h : -h, (o & 4) ? h : -h, P_MAX,
-               out + (size_t)i * hcount(P_MAX));
+  double2* dst = out + (size_t)i * (P_MAX + 1) * (P_MAX + 1);
+  double2 tmp[hcount(P_MAX)];
+  regular_half((o & 1) ? h : -h, (o & 2) ? h : -h, (o & 4) ? h : -h, P_MAX, tmp, rec);
+  for (int n = 0; n <= P_MAX; ++n)
+    for (int m = -n; m <= n; ++m) dst[n * n + n + m] = hget(tmp, n, m);
 }
 
 void build_rshift(const Tree& t, DevBuf<double2>& out, cudaStream_t s) {
@@ -128,8 +134,8 @@ void build_rshift(const Tree& t, DevBuf<double2>& out, cudaStream_t s) {
   for (int l = 0; l < t.n_levels; ++l) ch[l] = t.level_half[l];
   DevBuf<double> d;
   d.upload(ch, s);
-  out.resize((size_t)ch.size() * 8 * hcount(P_MAX));
-  k_rshift<<<grid_for(ch.size() * 8, 64), 64, 0, s>>>(d.get(), (int)ch.size(), out.get());
+  out.resize((size_t)ch.size() * 8 * (P_MAX + 1) * (P_MAX + 1));
+  k_rshift<<<grid_for(ch.size() * 8, 64), 64, 0, s>>>(d.get(), (int)ch.size(), out.get(), t.rec);
   FMM_LAUNCH_CHECK();
   FMM_CUDA(cudaStreamSynchronize(s));
 }
@@ -200,7 +206,10 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
   plan.n_crit = n_crit;
   plan.theta = theta;
   plan.max_depth = max_depth;
+  plan.recip.upload(make_recip_table(), s);
   build_trees(plan, src_xyz, ns, tgt_xyz, nt, s);
+  plan.src.rec = plan.recip.get();
+  plan.tgt.rec = plan.recip.get();
 
   std::vector<int2> m2l, p2p;
   traverse(plan, m2l, p2p, s);
@@ -277,11 +286,39 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
   plan.p2p_row.upload(plan.h_p2p_row, s);
   plan.p2p_src.upload(plan.h_p2p_src, s);
   std::vector<int> item_begin;
-  plan_make_items(T, S, plan.h_p2p_row, plan.h_p2p_src, 1024, plan.items, item_begin,
+  plan_make_items(T, S, plan.h_p2p_row, plan.h_p2p_src, 512, plan.items, item_begin,
                   plan.part_len, plan.p2p_interactions);
   plan.d_items.upload(plan.items, s);
   plan.tleaf_item_begin.upload(item_begin, s);
 
+  // needed(c): c is an M2L source or its parent's multipole is needed
+  {
+    std::vector<uint8_t> need(S.n_cells, 0), nz(T.n_cells, 0);
+    for (int sc : plan.h_m2l_src) need[sc] = 1;
+    for (int c = 1; c < S.n_cells; ++c)  // level-major numbering: parents come first
+      if (need[S.h_parent[c]]) need[c] = 1;
+    std::vector<int> cells;
+    plan.m2m_level_off.assign(1, 0);
+    for (int l = 0; l < S.n_levels; ++l) {
+      for (int c = S.level_start[l]; c < S.level_start[l + 1]; ++c)
+        if (!S.h_is_leaf[c] && need[c]) cells.push_back(c);
+      plan.m2m_level_off.push_back((int)cells.size());
+    }
+    plan.m2m_cells.upload(cells.empty() ? std::vector<int>(1, 0) : cells, s);
+    for (int c = 0; c < T.n_cells; ++c)
+      if (plan.h_m2l_row[c + 1] > plan.h_m2l_row[c]) nz[c] = 1;
+    for (int c = 1; c < T.n_cells; ++c)
+      if (nz[T.h_parent[c]]) nz[c] = 1;
+    cells.clear();
+    plan.l2l_level_off.assign(1, 0);
+    for (int l = 0; l < T.n_levels; ++l) {
+      if (l > 0)
+        for (int c = T.level_start[l]; c < T.level_start[l + 1]; ++c)
+          if (nz[T.h_parent[c]]) cells.push_back(c);
+      plan.l2l_level_off.push_back((int)cells.size());
+    }
+    plan.l2l_cells.upload(cells.empty() ? std::vector<int>(1, 0) : cells, s);
+  }
   build_rshift(S, plan.rshift_src, s);
   build_rshift(T, plan.rshift_tgt, s);
   FMM_CUDA(cudaStreamSynchronize(s));

@@ -1,0 +1,55 @@
+"""Multi-GPU host logic: one process per GPU (torch.distributed for the plumbing).
+
+Round-1 scope: ``bench.py`` runs N independent replicas (one per GPU) and
+reduces device times as max over ranks; the partitioned solve (target leaves
+split across GPUs, NCCL all-gather of source multipoles, all-reduce of the
+Arnoldi dots) builds on ``partition_contiguous`` below.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def partition_contiguous(weights, world: int) -> np.ndarray:
+    """Split items 0..n-1 (kept in order) into `world` contiguous ranges of ~equal weight.
+
+    Returns boundaries b (world+1,) with rank r owning [b[r], b[r+1]).  Every
+    rank computes the same split from the same weights (deterministic).
+    """
+    w = np.asarray(weights, dtype=np.float64)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    n = len(w)
+    c = np.concatenate([[0.0], np.cumsum(w)])
+    total = c[-1]
+    b = np.zeros(world + 1, dtype=np.int64)
+    b[world] = n
+    for r in range(1, world):
+        target = total * r / world
+        k = int(np.searchsorted(c, target, side="left"))
+        k = min(max(k, b[r - 1]), n)
+        # pick the closer of k-1 / k
+        if k > b[r - 1] and abs(c[k - 1] - target) <= abs(c[k] - target):
+            k -= 1
+        b[r] = k
+    return b
+
+
+def reduce_timing(local_ms: float, local_count: float, device=None):
+    """(max over ranks of the device time, sum over ranks of the work units).
+
+    Uses torch.distributed when it is initialised (nccl on GPUs, gloo in the
+    CPU tests); identity for a single process.
+    """
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(local_ms), float(local_count)
+    dev = device if device is not None else "cpu"
+    t = torch.tensor([float(local_ms)], dtype=torch.float64, device=dev)
+    n = torch.tensor([float(local_count)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(n, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(n.item())
