@@ -73,6 +73,11 @@ __device__ __forceinline__ double2 cfma_conj(double2 a, double2 b, double2 acc) 
   return acc;
 }
 
+// Full flat storage of operator tables (I grids, R grids): entry (N, c) at
+// N^2 + N + c, prefix-compatible in N.
+__host__ __device__ __forceinline__ int pidx(int N, int col) { return N * N + N + col; }
+__host__ __device__ __forceinline__ int tab_size(int order) { return (order + 1) * (order + 1); }
+
 // value of a half-stored real-symmetric expansion at (n, m), any sign of m
 __device__ __forceinline__ double2 hget(const double2* c, int n, int m) {
   if (m >= 0) return c[hidx(n, m)];

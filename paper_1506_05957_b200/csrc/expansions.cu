@@ -160,166 +160,4 @@ void launch_p2m(const TreeDev& S, const int* leaves, int n_leaves, int p, int C,
   throw ArgumentError("P2M: unsupported channel count");
 }
 
-// ------------------------------------------------------------------ M2M
-// One CTA per internal cell of a level.  All children's multipoles and the
-// R(d) of their octants are staged in FULL storage in shared memory, then
-// every (child, channel, coefficient) contribution is computed by its own
-// thread with branch-free index arithmetic (no per-child barriers), and the
-// children are summed in octant order.  Channels are processed in groups
-// small enough for shared memory.
-constexpr int VERT_THREADS = 256;
-constexpr int M2M_THREADS = 1024;
-constexpr size_t VERT_SMEM_BUDGET = 200 * 1024;
-
-__device__ __forceinline__ void expand_full(const double2* half, double2* full, int S, int tid,
-                                            int nthreads) {
-  for (int f = tid; f < S; f += nthreads) {
-    const int n = (int)sqrtf((float)f + 0.5f);
-    full[f] = hget(half, n, f - n * n - n);
-  }
-}
-
-__global__ void __launch_bounds__(M2M_THREADS)
-k_m2m(TreeDev S, const int* __restrict__ cells, int p, int Ctot, int cbase, int Ck,
-      const double2* __restrict__ rfull, double2* __restrict__ M) {
-  extern __shared__ double2 sh[];
-  const int cell = cells[blockIdx.x];
-  const int H = hcount(p), SF = (p + 1) * (p + 1), SP = (P_MAX + 1) * (P_MAX + 1);
-  const int fc = S.first_child[cell], nc = S.n_child[cell];
-  double2* sM = sh;                 // [8][Ck][SF]
-  double2* sR = sM + 8 * Ck * SF;   // [8][SF]
-  double2* sP = sR + 8 * SF;        // [8][Ck][H]
-  for (int ci = 0; ci < nc; ++ci) {
-    const int ch = fc + ci;
-    const int o = (S.cx[ch] > S.cx[cell] ? 1 : 0) | (S.cy[ch] > S.cy[cell] ? 2 : 0) |
-                  (S.cz[ch] > S.cz[cell] ? 4 : 0);
-    const double2* R = rfull + ((size_t)S.level[ch] * 8 + o) * SP;
-    for (int f = threadIdx.x; f < SF; f += blockDim.x) sR[ci * SF + f] = R[f];
-    for (int c = 0; c < Ck; ++c)
-      expand_full(M + ((size_t)ch * Ctot + cbase + c) * H, sM + (ci * Ck + c) * SF, SF, threadIdx.x,
-                  blockDim.x);
-  }
-  __syncthreads();
-  const int nw = nc * Ck * H;
-  for (int w = threadIdx.x; w < nw; w += blockDim.x) {
-    const int ci = w / (Ck * H), r = w - ci * Ck * H, c = r / H, idx = r - c * H;
-    const int n = c_n_of[idx], m = c_m_of[idx];
-    const double2* Mc = sM + (ci * Ck + c) * SF;
-    const double2* Rc = sR + ci * SF;
-    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-    for (int j = 0; j <= n; ++j) {
-      const int kmin = max(-j, m - (n - j)), kmax = min(j, m + (n - j));
-      const double2* Mrow = Mc + j * j + j;
-      const double2* Rrow = Rc + (n - j) * (n - j) + (n - j) + m;  // R_{n-j}^{m-k} = Rrow[-k]
-      int kk = kmin;
-      for (; kk + 1 <= kmax; kk += 2) {
-        a0 = cfma(Mrow[kk], Rrow[-kk], a0);
-        a1 = cfma(Mrow[kk + 1], Rrow[-kk - 1], a1);
-      }
-      if (kk <= kmax) a0 = cfma(Mrow[kk], Rrow[-kk], a0);
-    }
-    sP[w] = cadd(a0, a1);
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < Ck * H; t += blockDim.x) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int ci = 0; ci < nc; ++ci) s = cadd(s, sP[ci * Ck * H + t]);
-    const int c = t / H, idx = t - c * H;
-    M[((size_t)cell * Ctot + cbase + c) * H + idx] = s;
-  }
-}
-
-static int vert_group(int p, int C, int per_ck, int fixed) {
-  // largest channel group (<= C) whose shared-memory footprint fits the budget
-  for (int ck = C; ck >= 1; --ck)
-    if ((size_t)(per_ck * ck + fixed) * sizeof(double2) <= VERT_SMEM_BUDGET) return ck;
-  throw ArgumentError("expansion order too large for the M2M/L2L shared-memory tiles");
-}
-
-void launch_m2m(const TreeDev& S, const std::vector<int>& level_off, const int* cells, int p, int C,
-                const double2* rfull, double2* M, cudaStream_t st) {
-  const int H = hcount(p), SF = (p + 1) * (p + 1);
-  const int ckmax = vert_group(p, C, 8 * SF + 8 * H, 8 * SF);
-  static bool attr = false;
-  if (!attr) {
-    FMM_CUDA(cudaFuncSetAttribute(k_m2m, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)VERT_SMEM_BUDGET));
-    attr = true;
-  }
-  // level_off[l]..level_off[l+1]: parents at level l whose multipole is needed; deepest first
-  for (int l = (int)level_off.size() - 2; l >= 0; --l) {
-    const int a = level_off[l], b = level_off[l + 1];
-    if (b <= a) continue;
-    for (int cb = 0; cb < C; cb += ckmax) {
-      const int ck = std::min(ckmax, C - cb);
-      const size_t smem = (size_t)(8 * ck * SF + 8 * SF + 8 * ck * H) * sizeof(double2);
-      k_m2m<<<b - a, M2M_THREADS, smem, st>>>(S, cells + a, p, C, cb, ck, rfull, M);
-    }
-  }
-  FMM_LAUNCH_CHECK();
-}
-
-// ------------------------------------------------------------------ L2L
-// One CTA per cell of a level (>= 1): the parent's local expansion (full
-// storage) and R(child - parent) are staged in shared memory.
-__global__ void __launch_bounds__(VERT_THREADS)
-k_l2l(TreeDev T, const int* __restrict__ cells, int p, int Ctot, int cbase, int Ck,
-      const double2* __restrict__ rfull, double2* __restrict__ L) {
-  extern __shared__ double2 sh[];
-  const int cell = cells[blockIdx.x];
-  const int H = hcount(p), SF = (p + 1) * (p + 1), SP = (P_MAX + 1) * (P_MAX + 1);
-  const int par = T.parent[cell];
-  const int o = (T.cx[cell] > T.cx[par] ? 1 : 0) | (T.cy[cell] > T.cy[par] ? 2 : 0) |
-                (T.cz[cell] > T.cz[par] ? 4 : 0);
-  const double2* R = rfull + ((size_t)T.level[cell] * 8 + o) * SP;
-  double2* sL = sh;             // [Ck][SF]
-  double2* sR = sL + Ck * SF;   // [SF]
-  for (int f = threadIdx.x; f < SF; f += blockDim.x) sR[f] = R[f];
-  for (int c = 0; c < Ck; ++c)
-    expand_full(L + ((size_t)par * Ctot + cbase + c) * H, sL + c * SF, SF, threadIdx.x, blockDim.x);
-  __syncthreads();
-  for (int t = threadIdx.x; t < Ck * H; t += blockDim.x) {
-    const int c = t / H, idx = t - c * H;
-    const int n = c_n_of[idx], m = c_m_of[idx];
-    const double2* Lc = sL + c * SF;
-    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-    for (int j = n; j <= p; ++j) {
-      const int kmin = max(-j, m - (j - n)), kmax = min(j, m + (j - n));
-      const double2* Lrow = Lc + j * j + j;
-      const double2* Rrow = sR + (j - n) * (j - n) + (j - n) - m;  // R_{j-n}^{k-m} = Rrow[k]
-      int kk = kmin;
-      for (; kk + 1 <= kmax; kk += 2) {
-        a0 = cfma(Lrow[kk], Rrow[kk], a0);
-        a1 = cfma(Lrow[kk + 1], Rrow[kk + 1], a1);
-      }
-      if (kk <= kmax) a0 = cfma(Lrow[kk], Rrow[kk], a0);
-    }
-    double2* dst = L + ((size_t)cell * Ctot + cbase + c) * H + idx;
-    *dst = cadd(*dst, cadd(a0, a1));
-  }
-}
-
-void launch_l2l(const TreeDev& T, const std::vector<int>& level_off, const int* cells, int p, int C,
-                const double2* rfull, double2* L, cudaStream_t st) {
-  const int SF = (p + 1) * (p + 1);
-  const int ckmax = vert_group(p, C, SF, SF);
-  static bool attr = false;
-  if (!attr) {
-    FMM_CUDA(cudaFuncSetAttribute(k_l2l, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)VERT_SMEM_BUDGET));
-    attr = true;
-  }
-  // level_off[l]..level_off[l+1]: cells at level l whose parent carries a local expansion
-  for (int l = 1; l + 1 < (int)level_off.size(); ++l) {
-    const int a = level_off[l], b = level_off[l + 1];
-    if (b <= a) continue;
-    for (int cb = 0; cb < C; cb += ckmax) {
-      const int ck = std::min(ckmax, C - cb);
-      const size_t smem = (size_t)(ck * SF + SF) * sizeof(double2);
-      k_l2l<<<b - a, VERT_THREADS, smem, st>>>(T, cells + a, p, C, cb, ck, rfull, L);
-    }
-  }
-  FMM_LAUNCH_CHECK();
-}
-
 }  // namespace fmmbem

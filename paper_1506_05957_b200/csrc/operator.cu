@@ -354,13 +354,13 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s) {
       launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s);
     else
       launch_p2m(S, pl.src.leaves.get(), pl.src.n_leaves, c.p, C, q, d, op.M.get(), s);
-    launch_m2m(S, pl.m2m_level_off, pl.m2m_cells.get(), c.p, C, pl.rshift_src.get(), op.M.get(), s);
+    launch_m2m(pl.src, pl.m2m_level_off, pl.m2m_cells.get(), c.p, C, pl.rshift_src.get(), op.M.get(), s);
     record(op, ST_UP, true, s);
     record(op, ST_M2L, false, s);
     launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);
     record(op, ST_DOWN, false, s);
-    launch_l2l(T, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
+    launch_l2l(pl.tgt, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
     record(op, ST_DOWN, true, s);
   }
   FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
@@ -531,9 +531,9 @@ void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig
     DevBuf<double2> part((size_t)std::max<size_t>(plan.m2l_items.size(), 1) * C * hcount(p));
     launch_p2m(S, plan.src.leaves.get(), plan.src.n_leaves, p, C, q_orig ? qs.get() : nullptr,
                d_orig ? ds.get() : nullptr, M.get(), s);
-    launch_m2m(S, plan.m2m_level_off, plan.m2m_cells.get(), p, C, plan.rshift_src.get(), M.get(), s);
+    launch_m2m(plan.src, plan.m2m_level_off, plan.m2m_cells.get(), p, C, plan.rshift_src.get(), M.get(), s);
     launch_m2l(plan, p, C, M.get(), L.get(), part.get(), s);
-    launch_l2l(T, plan.l2l_level_off, plan.l2l_cells.get(), p, C, plan.rshift_tgt.get(), L.get(), s);
+    launch_l2l(plan.tgt, plan.l2l_level_off, plan.l2l_cells.get(), p, C, plan.rshift_tgt.get(), L.get(), s);
     launch_l2p_channels(T, plan.tgt.leaves.get(), plan.tgt.n_leaves, p, C, want_grad, L.get(), pot,
                         grad, s);
     FMM_CUDA(cudaStreamSynchronize(s));

@@ -26,6 +26,7 @@ struct Tree {
   DevBuf<uint8_t> is_leaf;
   // leaves in body order (device) and per sorted body its leaf cell
   DevBuf<int> leaves, leaf_of_body;
+  DevBuf<int> rtab;  // level * 8 + octant of each cell inside its parent (M2M/L2L table id)
   // sorted position -> original index, and sorted coordinates
   DevBuf<int> perm;
   DevBuf<double> px, py, pz;

@@ -1,0 +1,440 @@
+// Expansion translations (M2L, M2M, L2L) on one register-tiled engine.
+//
+// Reference operators (harmonics.py:156-218, applied in fmm.py:268-314):
+//   M2L  L_j^k  += (-1)^j sum_{n<=p,|m|<=n} M_n^m conj(I_{n+j}^{m+k}(D))   D = c_t - c_s
+//   M2M  M'_n^m += sum_{j<=n,k} M_j^k R_{n-j}^{m-k}(d)                     d = c_child - c_parent
+//   L2L  L'_n^m += sum_{j>=n,k} L_j^k R_{j-n}^{k-m}(d)                     d = c_child - c_parent
+// (the reference applies them as zgemm with dense (p+1)^2 x (p+1)^2 operators).
+//
+// One CTA owns one output expansion.  M2L / L2L: 4 warps stream the input
+// expansions ("pairs") through double-buffered shared memory - the operator
+// table (the full conj(I(D)) grid of order 2p, or the R(d) grid of order p)
+// arrives by cp.async while the previous pair is being contracted - and split
+// the input orders among themselves.  M2M: one warp per child, each with its
+// own buffer.  Lane l owns output order oc(l) and BJ consecutive output
+// degrees r0(l)..r0+BJ-1.
+// For a fixed input order, the table rows each lane needs slide by one row per
+// input degree, so every step is one shared-memory load of the operator, one
+// broadcast load of the input coefficient per channel, and BJ*CK complex FMAs;
+// the window rotates through registers by unrolling.  Warps are summed in a
+// fixed order at the end: deterministic, no atomics.  Outputs are half-stored
+// (m >= 0); inputs are expanded to full storage while staging.
+#include "kernels.cuh"
+
+namespace fmmbem {
+
+enum TMode : int { T_M2L = 0, T_M2M = 1, T_L2L = 2 };
+constexpr int TR_WARPS = 4;
+
+__host__ __device__ constexpr int tr_tiles(int p, int bj) {
+  int t = 0;
+  for (int k = 0; k <= p; ++k) t += (p - k + 1 + bj - 1) / bj;
+  return t;
+}
+__host__ __device__ constexpr int tr_bj(int p) {
+  int bj = 1;
+  while (tr_tiles(p, bj) > 32) ++bj;
+  return bj;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+struct TrArgs {
+  const int4* items;        // M2L: (out cell, pair begin, pair end, item id)
+  const int* cells;         // M2M / L2L: output cells
+  const int* pair_in;       // M2L: source cell per pair
+  const int* pair_tab;      // M2L: offset id per pair
+  const int* first_child;   // M2M
+  const int* n_child;       // M2M
+  const int* parent;        // L2L
+  const int* rtab;          // M2M / L2L: (level * 8 + octant) per cell
+  const double2* table;     // operator tables
+  int table_stride;         // complex per table entry
+  const double2* in;        // input expansions [cell][Ctot][H]
+  double2* out;             // M2L: partial blocks [item][Ctot][H]; else [cell][Ctot][H]
+  int Ctot, cbase;
+};
+
+template <int MODE> struct TrCfg {
+  static constexpr bool SPLIT_PAIRS = MODE == T_M2M;   // warp per input expansion
+  static constexpr int WARPS = MODE == T_M2M ? 8 : TR_WARPS;
+};
+
+template <int P, int CK, int MODE>
+__global__ void __launch_bounds__(TrCfg<MODE>::WARPS * 32) k_translate(TrArgs a) {
+  constexpr int BJ = tr_bj(P);
+  constexpr int H = (P + 1) * (P + 2) / 2;
+  constexpr int S = (P + 1) * (P + 1);
+  constexpr int TQ = MODE == T_M2L ? 2 * P : P;  // table order
+  constexpr bool SPLIT_PAIRS = TrCfg<MODE>::SPLIT_PAIRS;
+  constexpr int NW = TrCfg<MODE>::WARPS;
+  const int TT = tab_size(TQ);                    // entries copied per pair
+  // M2L reads rows up to 2p + BJ - 1 unclamped: rows past 2p only ever feed
+  // output degrees > p (discarded), so the slack rows are left uninitialised
+  const int TA = MODE == T_M2L ? tab_size(TQ + BJ) : TT;
+  const int BUF = TA + CK * S;
+  extern __shared__ double2 sh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- this CTA's output and its list of inputs
+  int out_cell, e0, e1, item_id = 0;
+  if (MODE == T_M2L) {
+    const int4 it = a.items[blockIdx.x];
+    out_cell = it.x;
+    e0 = it.y;
+    e1 = it.z;
+    item_id = it.w;
+  } else if (MODE == T_M2M) {
+    out_cell = a.cells[blockIdx.x];
+    e0 = a.first_child[out_cell];
+    e1 = e0 + a.n_child[out_cell];
+  } else {
+    out_cell = a.cells[blockIdx.x];
+    e0 = 0;
+    e1 = 1;
+  }
+  auto in_cell = [&](int e) {
+    return MODE == T_M2L ? a.pair_in[e] : MODE == T_M2M ? e : a.parent[out_cell];
+  };
+  auto tab_id = [&](int e) {
+    return MODE == T_M2L ? a.pair_tab[e] : MODE == T_M2M ? a.rtab[e] : a.rtab[out_cell];
+  };
+  // stage pair e into buf with `nthr` cooperating threads (thread index tid)
+  auto stage = [&](int e, double2* buf, int tid, int nthr) {
+    const double2* T = a.table + (size_t)tab_id(e) * a.table_stride;
+    for (int i = tid; i < TT; i += nthr) cp_async16(buf + i, T + i);
+    cp_async_commit();
+    const double2* src = a.in + ((size_t)in_cell(e) * a.Ctot + a.cbase) * H;
+    for (int f = tid; f < CK * S; f += nthr) {
+      const int c = f / S, g = f - c * S;
+      const int n = (int)__fsqrt_rz((float)g);
+      buf[TA + f] = hget(src + c * H, n, g - n * n - n);
+    }
+  };
+
+  // ---- lane tile, tile-major so that consecutive lanes hold consecutive oc
+  int oc = -1, r0 = 0;
+  {
+    int cum = 0;
+    for (int tau = 0; tau * BJ <= P; ++tau) {
+      const int nt = P - tau * BJ + 1;  // oc = 0 .. P - tau*BJ
+      if (oc < 0 && lane < cum + nt) {
+        oc = lane - cum;
+        r0 = oc + tau * BJ;
+      }
+      cum += nt;
+    }
+  }
+  const bool active = oc >= 0;
+  double2 acc[CK][BJ];
+#pragma unroll
+  for (int c = 0; c < CK; ++c)
+#pragma unroll
+    for (int t = 0; t < BJ; ++t) acc[c][t] = make_double2(0.0, 0.0);
+
+  // contract one staged pair over input orders am = -P + ai, ai = a0, a0 + astep, ...
+  auto contract = [&](const double2* sT, const double2* sIn, int a0, int astep) {
+    for (int ai = a0; ai < 2 * P + 1; ai += astep) {
+      const int am = ai - P;
+      const int b0 = am < 0 ? -am : am;
+      const int col = MODE == T_M2L ? am + oc : MODE == T_M2M ? oc - am : am - oc;
+      const int acol = col < 0 ? -col : col;
+      auto tval = [&](int row) -> double2 {  // M2M / L2L: masked, clamped
+        const int N = min(max(row, 0), TQ);
+        const double2 v = sT[pidx(N, max(min(col, N), -N))];
+        return row >= acol ? v : make_double2(0.0, 0.0);
+      };
+      double2 w[BJ];
+      int lead = 0, off = 0, dn = 0;
+      if (MODE == T_M2L) {
+        // rows b0 + r0 + t of conj(I); the entering row's offset is advanced incrementally
+#pragma unroll
+        for (int t = 0; t < BJ; ++t) w[t] = sT[pidx(b0 + r0 + t, col)];
+        lead = b0 + r0 + BJ;
+        off = pidx(lead, col);
+        dn = 2 * lead + 2;
+      } else if (MODE == T_M2M) {
+#pragma unroll
+        for (int t = 0; t < BJ; ++t) w[t] = tval(r0 + t - b0);
+        lead = r0 - b0 - 1;
+      } else {
+#pragma unroll
+        for (int t = 0; t < BJ; ++t) w[t] = tval(b0 - r0 - t);
+        lead = b0 + 1 - r0;
+      }
+      const double2* ip = sIn + b0 * b0 + b0 + am;
+      int istep = 2 * b0 + 2;
+      int b = b0;
+      auto step = [&](int q) {
+        double2 mv[CK];
+#pragma unroll
+        for (int c = 0; c < CK; ++c) mv[c] = ip[c * S];
+        ip += istep;
+        istep += 2;
+#pragma unroll
+        for (int t = 0; t < BJ; ++t) {
+          const int slot = MODE == T_M2L ? (q + t) % BJ : (t + BJ - q) % BJ;
+#pragma unroll
+          for (int c = 0; c < CK; ++c) acc[c][t] = cfma(mv[c], w[slot], acc[c][t]);
+        }
+        if (MODE == T_M2L) {
+          w[q] = sT[off];
+          off += dn;
+          dn += 2;
+        } else {
+          w[(BJ - 1 - q) % BJ] = tval(lead);
+          lead += MODE == T_M2M ? -1 : 1;
+        }
+      };
+      for (; b + BJ - 1 <= P; b += BJ) {
+        if (MODE == T_M2L) {
+          // issue the block's shared-memory loads first (inputs and entering
+          // operator rows), then run its BJ steps: hides the LDS latency
+          double2 mvb[BJ][CK], nw[BJ];
+#pragma unroll
+          for (int q = 0; q < BJ; ++q) {
+#pragma unroll
+            for (int c = 0; c < CK; ++c) mvb[q][c] = ip[c * S];
+            ip += istep;
+            istep += 2;
+            nw[q] = sT[off];
+            off += dn;
+            dn += 2;
+          }
+#pragma unroll
+          for (int q = 0; q < BJ; ++q) {
+#pragma unroll
+            for (int t = 0; t < BJ; ++t)
+#pragma unroll
+              for (int c = 0; c < CK; ++c) acc[c][t] = cfma(mvb[q][c], w[(q + t) % BJ], acc[c][t]);
+            w[q] = nw[q];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < BJ; ++q) step(q);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < BJ - 1; ++q)
+        if (b + q <= P) step(q);
+    }
+  };
+
+  if (SPLIT_PAIRS) {
+    double2* buf = sh + warp * BUF;
+    for (int e = e0 + warp; e < e1; e += NW) {
+      stage(e, buf, lane, 32);
+      cp_async_wait_all();
+      __syncwarp();
+      if (active) contract(buf, buf + TA, 0, 1);
+      __syncwarp();
+    }
+  } else {
+    if (e1 > e0) stage(e0, sh, threadIdx.x, blockDim.x);
+    for (int e = e0; e < e1; ++e) {
+      double2* cur = sh + ((e - e0) & 1) * BUF;
+      cp_async_wait_all();
+      __syncthreads();
+      if (e + 1 < e1) stage(e + 1, sh + ((e + 1 - e0) & 1) * BUF, threadIdx.x, blockDim.x);
+      if (active) contract(cur, cur + TA, warp, NW);
+    }
+  }
+  // ---- fixed-order reduction over the warps
+  __syncthreads();
+  double2* red = sh;  // [NW][32][CK][BJ]
+#pragma unroll
+  for (int c = 0; c < CK; ++c)
+#pragma unroll
+    for (int t = 0; t < BJ; ++t) red[((warp * 32 + lane) * CK + c) * BJ + t] = acc[c][t];
+  __syncthreads();
+  if (warp == 0 && active) {
+#pragma unroll
+    for (int c = 0; c < CK; ++c)
+#pragma unroll
+      for (int t = 0; t < BJ; ++t) {
+        const int r = r0 + t;
+        if (r > P) continue;
+        double2 s = red[(lane * CK + c) * BJ + t];
+        for (int w2 = 1; w2 < NW; ++w2) s = cadd(s, red[((w2 * 32 + lane) * CK + c) * BJ + t]);
+        const int idx = r * (r + 1) / 2 + oc;
+        if (MODE == T_M2L) {
+          if (r & 1) s = make_double2(-s.x, -s.y);
+          a.out[((size_t)item_id * a.Ctot + a.cbase + c) * H + idx] = s;
+        } else if (MODE == T_M2M) {
+          a.out[((size_t)out_cell * a.Ctot + a.cbase + c) * H + idx] = s;
+        } else {
+          double2* d = a.out + ((size_t)out_cell * a.Ctot + a.cbase + c) * H + idx;
+          *d = cadd(*d, s);
+        }
+      }
+  }
+}
+
+template <int P, int CK, int MODE>
+size_t tr_smem() {
+  constexpr int S = (P + 1) * (P + 1);
+  constexpr int TQ = MODE == T_M2L ? 2 * P : P;
+  const size_t one = (size_t)((MODE == T_M2L ? tab_size(TQ + tr_bj(P)) : tab_size(TQ)) + CK * S);
+  const size_t buf = TrCfg<MODE>::SPLIT_PAIRS ? TrCfg<MODE>::WARPS * one : 2 * one;
+  const size_t red = (size_t)TrCfg<MODE>::WARPS * 32 * CK * tr_bj(P);
+  return std::max(buf, red) * sizeof(double2);
+}
+
+template <int P, int CK, int MODE>
+void tr_launch_one(int nblocks, const TrArgs& a, cudaStream_t st) {
+  const size_t sm = tr_smem<P, CK, MODE>();
+  static bool attr = false;
+  if (!attr) {
+    FMM_CUDA(cudaFuncSetAttribute(k_translate<P, CK, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sm));
+    attr = true;
+  }
+  k_translate<P, CK, MODE><<<nblocks, TrCfg<MODE>::WARPS * 32, sm, st>>>(a);
+}
+
+template <int P, int MODE>
+void tr_launch_groups(int nblocks, TrArgs a, cudaStream_t st) {
+  constexpr size_t LIMIT = 227 * 1024;
+  // channel groups of 4 / 2 / 1 (Ctot = 1, 4 or 7), as large as shared memory allows
+  for (int cb = 0; cb < a.Ctot;) {
+    const int rem = a.Ctot - cb;
+    a.cbase = cb;
+    if (rem >= 4 && tr_smem<P, 4, MODE>() <= LIMIT) {
+      tr_launch_one<P, 4, MODE>(nblocks, a, st);
+      cb += 4;
+    } else if (rem >= 2 && tr_smem<P, 2, MODE>() <= LIMIT) {
+      tr_launch_one<P, 2, MODE>(nblocks, a, st);
+      cb += 2;
+    } else {
+      const bool fits = tr_smem<P, 1, MODE>() <= LIMIT;
+      FMM_REQUIRE(fits, "translation tiles exceed shared memory");
+      tr_launch_one<P, 1, MODE>(nblocks, a, st);
+      cb += 1;
+    }
+  }
+  FMM_LAUNCH_CHECK();
+}
+
+template <int MODE>
+void tr_dispatch(int p, int nblocks, const TrArgs& a, cudaStream_t st) {
+  if (nblocks <= 0) return;
+  switch (p) {
+#define TR_CASE(PP) case PP: tr_launch_groups<PP, MODE>(nblocks, a, st); break;
+    TR_CASE(0) TR_CASE(1) TR_CASE(2) TR_CASE(3) TR_CASE(4) TR_CASE(5) TR_CASE(6)
+    TR_CASE(7) TR_CASE(8) TR_CASE(9) TR_CASE(10) TR_CASE(11) TR_CASE(12) TR_CASE(13)
+    TR_CASE(14) TR_CASE(15) TR_CASE(16) TR_CASE(17) TR_CASE(18) TR_CASE(19) TR_CASE(20)
+#undef TR_CASE
+    default: throw ArgumentError("translation: expansion order out of range");
+  }
+}
+
+// ------------------------------------------------------------------ I grids (setup)
+// conj(I_n^m(D)) in FULL flat storage n^2+n+m for n <= order
+__global__ void k_igrid_full(const double* off, int n_off, int order, double2* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_off) return;
+  const double x = off[3 * i], y = off[3 * i + 1], z = off[3 * i + 2];
+  double2* o = out + (size_t)i * tab_size(order);
+  const double rho2 = x * x + y * y + z * z;
+  const double inv_r2 = 1.0 / rho2;
+  double2 diag = make_double2(1.0 / sqrt(rho2), 0.0);
+  auto put = [&](int n, int m, double2 v) {
+    // stored conjugated: the M2L contraction uses conj(I) (harmonics.py:180-198)
+    o[pidx(n, m)] = make_double2(v.x, -v.y);
+    if (m > 0) o[pidx(n, -m)] = (m & 1) ? make_double2(-v.x, -v.y) : v;
+  };
+  for (int m = 0; m <= order; ++m) {
+    if (m > 0) diag = cscale(cmul(make_double2(x, y), diag), -(2.0 * m - 1.0) * inv_r2);
+    put(m, m, diag);
+    if (m + 1 <= order) {
+      double2 prev2 = diag;
+      double2 prev1 = cscale(diag, (2.0 * m + 1.0) * z * inv_r2);
+      put(m + 1, m, prev1);
+      for (int n = m + 2; n <= order; ++n) {
+        const double aa = (2 * n - 1) * z;
+        const double bb = (double)((n - 1) * (n - 1) - m * m);
+        double2 cur;
+        cur.x = (aa * prev1.x - bb * prev2.x) * inv_r2;
+        cur.y = (aa * prev1.y - bb * prev2.y) * inv_r2;
+        put(n, m, cur);
+        prev2 = prev1;
+        prev1 = cur;
+      }
+    }
+  }
+}
+
+void compute_igrid_full(const double* d_off, int n_off, int order, double2* out, cudaStream_t s) {
+  if (n_off) k_igrid_full<<<grid_for(n_off, 64), 64, 0, s>>>(d_off, n_off, order, out);
+  FMM_LAUNCH_CHECK();
+}
+
+// L[cell] = sum of its M2L items' partial blocks (cells without items get zeros)
+__global__ void k_m2l_reduce(int n_cells, const int* __restrict__ cell_items, int CH,
+                             const double2* __restrict__ part, double2* __restrict__ L) {
+  const int cell = blockIdx.x;
+  const int i0 = cell_items[cell], i1 = cell_items[cell + 1];
+  for (int t = threadIdx.x; t < CH; t += blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int i = i0; i < i1; ++i) s = cadd(s, part[(size_t)i * CH + t]);
+    L[(size_t)cell * CH + t] = s;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
+                cudaStream_t st) {
+  TrArgs a{};
+  a.items = plan.d_m2l_items.get();
+  a.pair_in = plan.m2l_src.get();
+  a.pair_tab = plan.m2l_off.get();
+  a.table = plan.igrid.get();
+  a.table_stride = tab_size(2 * plan.igrid_p);
+  a.in = M;
+  a.out = part;
+  a.Ctot = C;
+  tr_dispatch<T_M2L>(p, (int)plan.m2l_items.size(), a, st);
+  k_m2l_reduce<<<plan.tgt.n_cells, 128, 0, st>>>(plan.tgt.n_cells, plan.m2l_cell_items.get(),
+                                                 C * hcount(p), part, L);
+  FMM_LAUNCH_CHECK();
+}
+
+void launch_m2m(const Tree& S, const std::vector<int>& level_off, const int* cells, int p, int C,
+                const double2* rfull, double2* M, cudaStream_t st) {
+  TrArgs a{};
+  a.first_child = S.first_child.get();
+  a.n_child = S.n_child.get();
+  a.rtab = S.rtab.get();
+  a.table = rfull;
+  a.table_stride = tab_size(P_MAX);
+  a.in = M;
+  a.out = M;
+  a.Ctot = C;
+  for (int l = (int)level_off.size() - 2; l >= 0; --l) {
+    a.cells = cells + level_off[l];
+    tr_dispatch<T_M2M>(p, level_off[l + 1] - level_off[l], a, st);
+  }
+}
+
+void launch_l2l(const Tree& T, const std::vector<int>& level_off, const int* cells, int p, int C,
+                const double2* rfull, double2* L, cudaStream_t st) {
+  TrArgs a{};
+  a.parent = T.parent.get();
+  a.rtab = T.rtab.get();
+  a.table = rfull;
+  a.table_stride = tab_size(P_MAX);
+  a.in = L;
+  a.out = L;
+  a.Ctot = C;
+  for (int l = 1; l + 1 < (int)level_off.size(); ++l) {
+    a.cells = cells + level_off[l];
+    tr_dispatch<T_L2L>(p, level_off[l + 1] - level_off[l], a, st);
+  }
+}
+
+}  // namespace fmmbem

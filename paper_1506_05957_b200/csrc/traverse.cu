@@ -121,11 +121,11 @@ __global__ void k_rshift(const double* child_half, int n_levels, double2* out,
   if (i >= n_levels * 8) return;
   const int l = i / 8, o = i % 8;
   const double h = child_half[l];
-  double2* dst = out + (size_t)i * (P_MAX + 1) * (P_MAX + 1);
+  double2* dst = out + (size_t)i * tab_size(P_MAX);
   double2 tmp[hcount(P_MAX)];
   regular_half((o & 1) ? h : -h, (o & 2) ? h : -h, (o & 4) ? h : -h, P_MAX, tmp, rec);
   for (int n = 0; n <= P_MAX; ++n)
-    for (int m = -n; m <= n; ++m) dst[n * n + n + m] = hget(tmp, n, m);
+    for (int m = -n; m <= n; ++m) dst[pidx(n, m)] = hget(tmp, n, m);
 }
 
 void build_rshift(const Tree& t, DevBuf<double2>& out, cudaStream_t s) {
@@ -134,7 +134,7 @@ void build_rshift(const Tree& t, DevBuf<double2>& out, cudaStream_t s) {
   for (int l = 0; l < t.n_levels; ++l) ch[l] = t.level_half[l];
   DevBuf<double> d;
   d.upload(ch, s);
-  out.resize((size_t)ch.size() * 8 * (P_MAX + 1) * (P_MAX + 1));
+  out.resize((size_t)ch.size() * 8 * tab_size(P_MAX));
   k_rshift<<<grid_for(ch.size() * 8, 64), 64, 0, s>>>(d.get(), (int)ch.size(), out.get(), t.rec);
   FMM_LAUNCH_CHECK();
   FMM_CUDA(cudaStreamSynchronize(s));
@@ -190,7 +190,7 @@ void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s) {
   FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
   if (plan.igrid_p >= p) return;
   const int order = 2 * p;
-  plan.igrid.resize((size_t)std::max(plan.n_offsets, 1) * (order + 1) * (order + 1));
+  plan.igrid.resize((size_t)std::max(plan.n_offsets, 1) * tab_size(order));
   compute_igrid_full(plan.off_d.get(), plan.n_offsets, order, plan.igrid.get(), s);
   FMM_CUDA(cudaStreamSynchronize(s));
   plan.igrid_p = p;
@@ -318,6 +318,16 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
       plan.l2l_level_off.push_back((int)cells.size());
     }
     plan.l2l_cells.upload(cells.empty() ? std::vector<int>(1, 0) : cells, s);
+  }
+  for (Tree* tr : {&plan.src, &plan.tgt}) {
+    std::vector<int> rt(tr->n_cells, 0);
+    for (int c = 1; c < tr->n_cells; ++c) {
+      const int pa = tr->h_parent[c];
+      const int o = (tr->h_cx[c] > tr->h_cx[pa] ? 1 : 0) | (tr->h_cy[c] > tr->h_cy[pa] ? 2 : 0) |
+                    (tr->h_cz[c] > tr->h_cz[pa] ? 4 : 0);
+      rt[c] = tr->h_level[c] * 8 + o;
+    }
+    tr->rtab.upload(rt, s);
   }
   build_rshift(S, plan.rshift_src, s);
   build_rshift(T, plan.rshift_tgt, s);

@@ -1,0 +1,101 @@
+"""GPU, full-size configs (BASELINE.json configs 4 and 5): parity on the reference's
+sampled goldens (tools/make_goldens_large.py) plus size-independent properties."""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+_OPS = {}
+
+
+def _op(name):
+    from paper_1506_05957_b200.configs import CONFIGS
+    from paper_1506_05957_b200.operator import GpuBemOperator
+
+    if name not in _OPS:
+        cfg = CONFIGS[name]
+        _OPS[name] = (GpuBemOperator(cfg.mesh(), cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit,
+                                     mu=cfg.mu), cfg)
+    return _OPS[name]
+
+
+def _sampled(name):
+    path = os.path.join(GOLDEN, f"{name}_sampled.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{name}_sampled.npz not generated")
+    return load_golden(f"{name}_sampled")
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg4"])
+def test_fullsize_apply_matches_reference_samples(name):
+    g = _sampled(name)
+    op, cfg = _op(name)
+    assert hashlib.sha256(op.src_pos.tobytes()).hexdigest() == str(g["src_pos_sha256"])
+    rows = g["rows"]
+    x = np.random.default_rng(1).uniform(-1.0, 1.0, op.shape[0])
+    for p in (cfg.p_min, cfg.p_initial):
+        y = op.apply(x, p)
+        assert rel_l2(y[rows], g[f"apply_p{p}_rows"]) <= 1e-10, p
+        assert abs(np.linalg.norm(y) / float(g[f"apply_p{p}_norm"]) - 1.0) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg4"])
+def test_fullsize_rhs_matches_reference_samples(name):
+    g = _sampled(name)
+    op, cfg = _op(name)
+    b = op.assemble_rhs(cfg.boundary_data(op.centroids, op.normals))
+    assert rel_l2(b[g["rows"]], g["rhs_rows"]) <= 1e-10
+    assert abs(np.linalg.norm(b) / float(g["rhs_norm"]) - 1.0) <= 1e-10
+
+
+def test_cfg5_relaxed_gmres_matches_reference():
+    from paper_1506_05957_b200.solver import solve
+
+    g = _sampled("cfg5")
+    op, cfg = _op("cfg5")
+    b = op.assemble_rhs(cfg.boundary_data(op.centroids, op.normals))
+    res = solve(op, b, eta=cfg.tol, p_initial=cfg.p_initial, p_min=cfg.p_min, relaxed=True,
+                max_iter=cfg.max_iter)
+    ref = g["relaxed_orders"].tolist()
+    assert abs(res.n_iterations - len(ref)) <= 1
+    assert res.orders[:min(len(ref), res.n_iterations)] == ref[:min(len(ref), res.n_iterations)]
+    assert rel_l2(res.x[g["rows"]], g["relaxed_x_rows"]) <= 1e-6
+    ex = cfg.exact_potential(op.centroids)
+    err = np.linalg.norm(res.x - ex) / np.linalg.norm(ex)
+    assert abs(err - float(g["relaxed_err_exact"])) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg4"])
+def test_fullsize_linearity_and_determinism(name):
+    op, cfg = _op(name)
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, op.shape[0])
+    z = rng.uniform(-1, 1, op.shape[0])
+    p = cfg.p_initial
+    ax, az = op.apply(x, p), op.apply(z, p)
+    assert rel_l2(op.apply(x + 2.0 * z, p), ax + 2.0 * az) <= 1e-12
+    assert np.array_equal(op.apply(x, p), ax)  # bitwise reproducible (no atomics)
+
+
+@pytest.mark.parametrize("name", ["cfg5", "cfg4"])
+def test_fullsize_traversal_accounts_every_source(name):
+    """Every target sees every source exactly once through the M2L/P2P lists
+    (the reference's test_fmm.py:33-39 property), at full size."""
+    op, _ = _op(name)
+    counts = op.plan.interaction_counts()
+    assert np.all(counts == len(op.src_pos))
+
+
+def test_fullsize_error_decreases_with_p():
+    op, cfg = _op("cfg5")
+    x = np.random.default_rng(5).uniform(-1, 1, op.shape[0])
+    ref = op.apply(x, 18)
+    errs = [rel_l2(op.apply(x, p), ref) for p in (3, 6, 9, 12)]
+    assert all(a > b for a, b in zip(errs, errs[1:]))
+    assert errs[-1] < 1e-6

@@ -14,7 +14,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                       "-k", f"regex:{kern}", "--launch-skip", skip, "--launch-count", "1"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-h = rows[1]
+h = rows[1] if len(rows) > 1 else sys.exit("no rows")
 data = [r for r in rows[2:] if len(r) == len(h)]
 si = h.index("Warp Stall Sampling (All Samples)")
 src = h.index("Source")
