@@ -230,7 +230,7 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
     op.part.ensure((size_t)std::max<int64_t>(op.plan.part_len, 1) * 3);
     op.M.ensure((size_t)op.plan.src.n_cells * C * hcount(p));
     op.L.ensure((size_t)op.plan.tgt.n_cells * C * hcount(p));
-    op.m2l_part.ensure((size_t)std::max<size_t>(op.plan.m2l_items.size(), 1) * C * hcount(p));
+    op.m2l_part.ensure((size_t)std::max(op.plan.n_m2l, 1) * C * hcount(p));
     plan_ensure_igrid(op.plan, p, op.s_main);
     if (kind == op.basis_kind_for_sys) op.use_basis = ensure_p2m_basis(op, p, op.s_main);
   }
@@ -528,7 +528,7 @@ void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig
   if (parts & 1) {
     plan_ensure_igrid(plan, p, s);
     DevBuf<double2> M((size_t)plan.src.n_cells * C * hcount(p)), L((size_t)plan.tgt.n_cells * C * hcount(p));
-    DevBuf<double2> part((size_t)std::max<size_t>(plan.m2l_items.size(), 1) * C * hcount(p));
+    DevBuf<double2> part((size_t)std::max(plan.n_m2l, 1) * C * hcount(p));
     launch_p2m(S, plan.src.leaves.get(), plan.src.n_leaves, p, C, q_orig ? qs.get() : nullptr,
                d_orig ? ds.get() : nullptr, M.get(), s);
     launch_m2m(plan.src, plan.m2m_level_off, plan.m2m_cells.get(), p, C, plan.rshift_src.get(), M.get(), s);

@@ -70,6 +70,11 @@ struct Plan {
   std::vector<int4> m2l_items;
   DevBuf<int4> d_m2l_items;
   DevBuf<int> m2l_cell_items;  // n_tgt_cells + 1 offsets into m2l_items
+  // offset-grouped M2L: pairs (CSR positions) sorted by offset, items of <= 8
+  // pairs sharing one translation (off id, begin, end into m2l_gpair)
+  std::vector<int4> m2l_gitems;
+  DevBuf<int4> d_m2l_gitems;
+  DevBuf<int> m2l_gpair;
   std::vector<int> m2l_tgt_cells;  // target cells with >= 1 M2L source
   DevBuf<int> d_m2l_tgt_cells;
 

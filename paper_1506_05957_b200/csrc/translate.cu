@@ -61,8 +61,9 @@ struct TrArgs {
 };
 
 template <int MODE> struct TrCfg {
-  static constexpr bool SPLIT_PAIRS = MODE == T_M2M;   // warp per input expansion
-  static constexpr int WARPS = MODE == T_M2M ? 8 : TR_WARPS;
+  static constexpr bool SPLIT_PAIRS = MODE == T_M2M;   // warps per input expansion (child)
+  static constexpr int MSPLIT = MODE == T_M2M ? 2 : 1;  // warps sharing one child
+  static constexpr int WARPS = MODE == T_M2M ? 16 : TR_WARPS;
 };
 
 template <int P, int CK, int MODE>
@@ -226,14 +227,13 @@ __global__ void __launch_bounds__(TrCfg<MODE>::WARPS * 32) k_translate(TrArgs a)
   };
 
   if (SPLIT_PAIRS) {
-    double2* buf = sh + warp * BUF;
-    for (int e = e0 + warp; e < e1; e += NW) {
-      stage(e, buf, lane, 32);
-      cp_async_wait_all();
-      __syncwarp();
-      if (active) contract(buf, buf + TA, 0, 1);
-      __syncwarp();
-    }
+    // every child staged at once (<= 8), then MSPLIT warps per child split its input orders
+    constexpr int MS = TrCfg<MODE>::MSPLIT;
+    for (int e = e0; e < e1; ++e) stage(e, sh + (e - e0) * BUF, threadIdx.x, blockDim.x);
+    cp_async_wait_all();
+    __syncthreads();
+    const int g = warp / MS;
+    if (active && e0 + g < e1) contract(sh + g * BUF, sh + g * BUF + TA, warp % MS, MS);
   } else {
     if (e1 > e0) stage(e0, sh, threadIdx.x, blockDim.x);
     for (int e = e0; e < e1; ++e) {
@@ -280,7 +280,7 @@ size_t tr_smem() {
   constexpr int S = (P + 1) * (P + 1);
   constexpr int TQ = MODE == T_M2L ? 2 * P : P;
   const size_t one = (size_t)((MODE == T_M2L ? tab_size(TQ + tr_bj(P)) : tab_size(TQ)) + CK * S);
-  const size_t buf = TrCfg<MODE>::SPLIT_PAIRS ? TrCfg<MODE>::WARPS * one : 2 * one;
+  const size_t buf = TrCfg<MODE>::SPLIT_PAIRS ? 8 * one : 2 * one;
   const size_t red = (size_t)TrCfg<MODE>::WARPS * 32 * CK * tr_bj(P);
   return std::max(buf, red) * sizeof(double2);
 }
@@ -386,21 +386,207 @@ __global__ void k_m2l_reduce(int n_cells, const int* __restrict__ cell_items, in
   }
 }
 
+// ------------------------------------------------------------------ M2L, offset-grouped
+// One CTA per (translation offset, <= 8 pairs): the conj(I(D)) grid is staged
+// once and applied to NV = 4 input vectors at a time (4 pairs x 1 channel, or
+// 1 pair x 4 channels), so every gathered operator value feeds 4*BJ complex
+// FMAs; the 4 warps split the input orders.  Each pair's result is written to
+// its CSR slot and a second kernel adds a target's pairs in CSR order
+// (deterministic).
+template <int P, int CK>
+__global__ void __launch_bounds__(TR_WARPS * 32)
+k_m2l_grouped(const int4* __restrict__ items, const int* __restrict__ gpair,
+              const int* __restrict__ pair_src, const double2* __restrict__ table, int table_stride,
+              const double2* __restrict__ M, int Ctot, int cbase, double2* __restrict__ pout) {
+  constexpr int BJ = tr_bj(P);
+  constexpr int H = (P + 1) * (P + 2) / 2;
+  constexpr int S = (P + 1) * (P + 1);
+  constexpr int TQ = 2 * P;
+  constexpr int NV = 4;            // vectors per contraction pass
+  constexpr int NP = NV / CK;      // pairs per pass
+  const int TT = tab_size(TQ), TA = tab_size(TQ + BJ);
+  extern __shared__ double2 sh[];
+  double2* sT = sh;
+  double2* sM = sh + TA;           // [NV][S]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 it = items[blockIdx.x];
+  {
+    const double2* T = table + (size_t)it.x * table_stride;
+    for (int i = threadIdx.x; i < TT; i += blockDim.x) cp_async16(sT + i, T + i);
+    cp_async_commit();
+  }
+  int oc = -1, r0 = 0;
+  {
+    int cum = 0;
+    for (int kk = 0; kk <= P; ++kk) {
+      const int nt = (P - kk + 1 + BJ - 1) / BJ;
+      if (oc < 0 && lane < cum + nt) {
+        oc = kk;
+        r0 = kk + (lane - cum) * BJ;
+      }
+      cum += nt;
+    }
+  }
+  const bool active = oc >= 0;
+  for (int e0 = it.y; e0 < it.z; e0 += NP) {
+    const int np = min(NP, it.z - e0);
+    const int nv = np * CK;
+    __syncthreads();  // previous pass done with sM
+    for (int f = threadIdx.x; f < NV * S; f += blockDim.x) {
+      const int v = f / S, g = f - v * S;
+      double2 val = make_double2(0.0, 0.0);
+      if (v < nv) {
+        const int e = gpair[e0 + v / CK], c = cbase + v % CK;
+        const int n = (int)__fsqrt_rz((float)g);
+        val = hget(M + ((size_t)pair_src[e] * Ctot + c) * H, n, g - n * n - n);
+      }
+      sM[f] = val;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    double2 acc[NV][BJ];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int t = 0; t < BJ; ++t) acc[v][t] = make_double2(0.0, 0.0);
+    if (active) {
+      for (int ai = warp; ai < 2 * P + 1; ai += TR_WARPS) {
+        const int am = ai - P;
+        const int b0 = am < 0 ? -am : am;
+        const int col = am + oc;
+        double2 w[BJ];
+#pragma unroll
+        for (int t = 0; t < BJ; ++t) w[t] = sT[pidx(b0 + r0 + t, col)];
+        int off = pidx(b0 + r0 + BJ, col), dn = 2 * (b0 + r0 + BJ) + 2;
+        const double2* ip = sM + b0 * b0 + b0 + am;
+        int istep = 2 * b0 + 2;
+        auto step = [&](int q) {
+          double2 mv[NV];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) mv[v] = ip[v * S];
+          const double2 nw = sT[off];
+          ip += istep;
+          istep += 2;
+          off += dn;
+          dn += 2;
+#pragma unroll
+          for (int t = 0; t < BJ; ++t)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v][t] = cfma(mv[v], w[(q + t) % BJ], acc[v][t]);
+          w[q] = nw;
+        };
+        int b = b0;
+        for (; b + BJ - 1 <= P; b += BJ) {
+#pragma unroll
+          for (int q = 0; q < BJ; ++q) step(q);
+        }
+#pragma unroll
+        for (int q = 0; q < BJ - 1; ++q)
+          if (b + q <= P) step(q);
+      }
+    }
+    // fixed-order reduction over the 4 warps, one vector at a time
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      __syncthreads();
+      double2* red = sM;  // reuse: [4 warps][32][BJ] <= NV * S
+#pragma unroll
+      for (int t = 0; t < BJ; ++t) red[(warp * 32 + lane) * BJ + t] = acc[v][t];
+      __syncthreads();
+      if (warp == 0 && active && v < nv) {
+        const int e = gpair[e0 + v / CK], c = cbase + v % CK;
+#pragma unroll
+        for (int t = 0; t < BJ; ++t) {
+          const int r = r0 + t;
+          if (r > P) continue;
+          double2 sum = red[lane * BJ + t];
+          for (int w2 = 1; w2 < TR_WARPS; ++w2) sum = cadd(sum, red[(w2 * 32 + lane) * BJ + t]);
+          if (r & 1) sum = make_double2(-sum.x, -sum.y);
+          pout[((size_t)e * Ctot + c) * H + r * (r + 1) / 2 + oc] = sum;
+        }
+      }
+    }
+  }
+}
+
+// L[cell] = sum over the cell's M2L pairs (CSR order) of their results
+__global__ void k_m2l_gather(int n_cells, const int* __restrict__ row, int CH,
+                             const double2* __restrict__ pout, double2* __restrict__ L) {
+  const int cell = blockIdx.x;
+  const int i0 = row[cell], i1 = row[cell + 1];
+  for (int t = threadIdx.x; t < CH; t += blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int i = i0; i < i1; ++i) s = cadd(s, pout[(size_t)i * CH + t]);
+    L[(size_t)cell * CH + t] = s;
+  }
+}
+
+template <int P, int CK>
+size_t m2lg_smem() {
+  constexpr int S = (P + 1) * (P + 1);
+  const size_t red = (size_t)TR_WARPS * 32 * tr_bj(P);
+  return ((size_t)tab_size(2 * P + tr_bj(P)) + std::max((size_t)4 * S, red)) * sizeof(double2);
+}
+
+template <int P>
+void m2lg_launch(const Plan& plan, int C, const double2* M, double2* pout, cudaStream_t st) {
+  const int n = (int)plan.m2l_gitems.size();
+  if (!n) return;
+  const int stride = tab_size(2 * plan.igrid_p);
+  for (int cb = 0; cb < C;) {
+    const int rem = C - cb;
+    if (rem >= 4) {
+      static bool a4 = false;
+      if (!a4) {
+        FMM_CUDA(cudaFuncSetAttribute(k_m2l_grouped<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)m2lg_smem<P, 4>()));
+        a4 = true;
+      }
+      k_m2l_grouped<P, 4><<<n, TR_WARPS * 32, m2lg_smem<P, 4>(), st>>>(
+          plan.d_m2l_gitems.get(), plan.m2l_gpair.get(), plan.m2l_src.get(), plan.igrid.get(), stride,
+          M, C, cb, pout);
+      cb += 4;
+    } else if (rem >= 2) {
+      static bool a2 = false;
+      if (!a2) {
+        FMM_CUDA(cudaFuncSetAttribute(k_m2l_grouped<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)m2lg_smem<P, 2>()));
+        a2 = true;
+      }
+      k_m2l_grouped<P, 2><<<n, TR_WARPS * 32, m2lg_smem<P, 2>(), st>>>(
+          plan.d_m2l_gitems.get(), plan.m2l_gpair.get(), plan.m2l_src.get(), plan.igrid.get(), stride,
+          M, C, cb, pout);
+      cb += 2;
+    } else {
+      static bool a1 = false;
+      if (!a1) {
+        FMM_CUDA(cudaFuncSetAttribute(k_m2l_grouped<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)m2lg_smem<P, 1>()));
+        a1 = true;
+      }
+      k_m2l_grouped<P, 1><<<n, TR_WARPS * 32, m2lg_smem<P, 1>(), st>>>(
+          plan.d_m2l_gitems.get(), plan.m2l_gpair.get(), plan.m2l_src.get(), plan.igrid.get(), stride,
+          M, C, cb, pout);
+      cb += 1;
+    }
+  }
+  FMM_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------------------ launchers
 void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
                 cudaStream_t st) {
-  TrArgs a{};
-  a.items = plan.d_m2l_items.get();
-  a.pair_in = plan.m2l_src.get();
-  a.pair_tab = plan.m2l_off.get();
-  a.table = plan.igrid.get();
-  a.table_stride = tab_size(2 * plan.igrid_p);
-  a.in = M;
-  a.out = part;
-  a.Ctot = C;
-  tr_dispatch<T_M2L>(p, (int)plan.m2l_items.size(), a, st);
-  k_m2l_reduce<<<plan.tgt.n_cells, 128, 0, st>>>(plan.tgt.n_cells, plan.m2l_cell_items.get(),
-                                                 C * hcount(p), part, L);
+  // part holds one result block per M2L pair (CSR order): n_m2l * C * hcount(p)
+  switch (p) {
+#define G_CASE(PP) case PP: m2lg_launch<PP>(plan, C, M, part, st); break;
+    G_CASE(0) G_CASE(1) G_CASE(2) G_CASE(3) G_CASE(4) G_CASE(5) G_CASE(6)
+    G_CASE(7) G_CASE(8) G_CASE(9) G_CASE(10) G_CASE(11) G_CASE(12) G_CASE(13)
+    G_CASE(14) G_CASE(15) G_CASE(16) G_CASE(17) G_CASE(18) G_CASE(19) G_CASE(20)
+#undef G_CASE
+    default: throw ArgumentError("M2L: expansion order out of range");
+  }
+  k_m2l_gather<<<plan.tgt.n_cells, 128, 0, st>>>(plan.tgt.n_cells, plan.m2l_row.get(), C * hcount(p),
+                                                 part, L);
   FMM_LAUNCH_CHECK();
 }
 

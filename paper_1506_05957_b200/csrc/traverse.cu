@@ -273,6 +273,25 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
   cell_items[T.n_cells] = (int)plan.m2l_items.size();
   plan.d_m2l_items.upload(plan.m2l_items, s);
   plan.m2l_cell_items.upload(cell_items, s);
+  {
+    // offset-grouped work: pairs sharing a translation share its operator grid
+    std::vector<int> gp(m2l.size());
+    for (size_t k = 0; k < gp.size(); ++k) gp[k] = (int)k;
+    std::stable_sort(gp.begin(), gp.end(), [&](int a, int b) { return offid[a] < offid[b]; });
+    plan.m2l_gitems.clear();
+    for (size_t i = 0; i < gp.size();) {
+      size_t j = i;
+      while (j < gp.size() && offid[gp[j]] == offid[gp[i]]) ++j;
+      const int len = (int)(j - i), nch = (len + 7) / 8;
+      for (int q = 0; q < nch; ++q) {
+        const int lo = (int)i + (int)((int64_t)len * q / nch), hi = (int)i + (int)((int64_t)len * (q + 1) / nch);
+        plan.m2l_gitems.push_back(make_int4(offid[gp[i]], lo, hi, 0));
+      }
+      i = j;
+    }
+    plan.d_m2l_gitems.upload(plan.m2l_gitems.empty() ? std::vector<int4>(1) : plan.m2l_gitems, s);
+    plan.m2l_gpair.upload(gp.empty() ? std::vector<int>(1, 0) : gp, s);
+  }
 
   // P2P CSR by target leaf and the balanced work items
   plan.n_p2p = (int)p2p.size();
