@@ -130,6 +130,22 @@ int fmmbem_op_stage_times(fmmbem_op* op, double* ms6, int64_t* calls, int reset)
 int fmmbem_op_counters(fmmbem_op* op, int64_t* kernel_launches, int64_t* applies,
                        double* last_call_ms);
 
+/* ---------------------------------------------------------------- multi-GPU (one process per GPU)
+ * rank r owns target leaves [tleaf_bounds[r], tleaf_bounds[r+1]) and source
+ * leaves [sleaf_bounds[r], sleaf_bounds[r+1]) (leaf indices in body order, bounds of length
+ * world+1).  Each apply does P2M of its source leaves, an NCCL all-gather of the leaf
+ * multipoles, M2L/L2L/P2P/epilogue for its target leaves and an NCCL all-gather of the
+ * result; GMRES then runs replicated.  nccl_id: 128 bytes from fmmbem_nccl_unique_id on rank
+ * 0, shared by the caller (e.g. torch.distributed); NULL = "virtual" shard without
+ * collectives that computes only its own rows (single-GPU check of the work split). */
+int fmmbem_nccl_unique_id(unsigned char* out128);
+/* per-leaf work weights (which = 0 target leaves: P2P + M2L flop estimate; 1 source leaves:
+ * bodies), leaf order = body order, for the host-side partitioner */
+int fmmbem_op_leaf_work(const fmmbem_op* op, int which, double* w);
+int fmmbem_op_shard(fmmbem_op* op, int rank, int world, const int32_t* tleaf_bounds,
+                    const int32_t* sleaf_bounds, const unsigned char* nccl_id);
+int fmmbem_op_unshard(fmmbem_op* op);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,11 @@ SIGNATURES = {
     "fmmbem_op_set_timing": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int]),
     "fmmbem_op_stage_times": (ctypes.c_int, [_vp, _c_double_p, _c_int64_p, ctypes.c_int]),
     "fmmbem_op_counters": (ctypes.c_int, [_vp, _c_int64_p, _c_int64_p, _c_double_p]),
+    "fmmbem_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "fmmbem_op_leaf_work": (ctypes.c_int, [_vp, ctypes.c_int, _c_double_p]),
+    "fmmbem_op_shard": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _c_int32_p, _c_int32_p,
+                                       ctypes.c_char_p]),
+    "fmmbem_op_unshard": (ctypes.c_int, [_vp]),
 }
 
 _lib = None

@@ -430,6 +430,42 @@ int fmmbem_op_stage_times(fmmbem_op* h, double* ms6, int64_t* calls, int reset) 
   });
 }
 
+int fmmbem_nccl_unique_id(unsigned char* out128) {
+  return guarded([&] {
+    FMM_REQUIRE(out128, "null argument");
+    nccl_unique_id(out128);
+  });
+}
+
+int fmmbem_op_leaf_work(const fmmbem_op* h, int which, double* w) {
+  return guarded([&] {
+    FMM_REQUIRE(h && w && (which == 0 || which == 1), "bad arguments");
+    op_leaf_work(*h->op, which, w);
+  });
+}
+
+int fmmbem_op_shard(fmmbem_op* h, int rank, int world, const int32_t* tleaf_bounds,
+                    const int32_t* sleaf_bounds, const unsigned char* nccl_id) {
+  return guarded([&] {
+    FMM_REQUIRE(h && tleaf_bounds && sleaf_bounds, "null argument");
+    select(h->device);
+    op_shard_setup(*h->op, rank, world, tleaf_bounds, sleaf_bounds, nccl_id);
+  });
+}
+
+int fmmbem_op_unshard(fmmbem_op* h) {
+  return guarded([&] {
+    FMM_REQUIRE(h, "null argument");
+    select(h->device);
+    op_shard_release(*h->op);
+    BemOp& op = *h->op;
+    for (auto& kv : op.graphs) cudaGraphExecDestroy(kv.second);
+    op.graphs.clear();
+    op.graph_kernels.clear();
+    op.graph_sig.clear();
+  });
+}
+
 int fmmbem_op_counters(fmmbem_op* h, int64_t* kernel_launches, int64_t* applies,
                        double* last_call_ms) {
   return guarded([&] {

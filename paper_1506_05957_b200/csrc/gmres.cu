@@ -126,6 +126,8 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   FMM_REQUIRE(tol > 0.0, "eta must be positive");
   FMM_REQUIRE(max_iter >= 0, "max_iter must be >= 0");
   FMM_REQUIRE(p_initial >= 0 && p_initial <= P_MAX, "p_initial must be in [0, 20]");
+  FMM_REQUIRE(!(op.shard.active && op.shard.virtual_mode),
+              "GMRES needs full mat-vecs: a virtual shard only computes its own rows");
   GmresResult res;
   const int64_t n = op.n;
   cudaStream_t s = op.s_main;

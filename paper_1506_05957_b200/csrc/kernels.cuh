@@ -31,8 +31,10 @@ void launch_p2m(const TreeDev& S, const int* leaves, int n_leaves, int p, int C,
 void launch_m2m(const Tree& S, const std::vector<int>& level_off, const int* cells, int p, int C,
                 const double2* rfull, double2* M, cudaStream_t st);
 // M2L into per-item partial blocks (part: n_items * C * hcount(p)) then reduced into L (all cells)
+// (gitems, cells: optional restricted work lists for a shard; defaults = whole plan)
 void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
-                cudaStream_t st);
+                cudaStream_t st, const int4* gitems = nullptr, int n_gitems = -1,
+                const int* cells = nullptr, int n_cells = -1, const int* gpair = nullptr);
 void compute_igrid_full(const double* d_off, int n_off, int order, double2* out, cudaStream_t s);
 // L2L into the cells listed per level whose parent has a nonzero local expansion
 void launch_l2l(const Tree& T, const std::vector<int>& level_off, const int* cells, int p, int C,

@@ -97,6 +97,8 @@ struct EpiArgs {
   const double* x;
   double alpha, beta;
   double* y;
+  double* ysorted;  // sharded: write (target body - tbody_a) * NC + c instead of y[panel]
+  int tbody_a;
 };
 
 template <int KIND, bool FAR>
@@ -134,7 +136,9 @@ __global__ void __launch_bounds__(128) k_epilogue(TreeDev T, EpiArgs a) {
       double corr = 0.0;
       for (int e = a.rowptr[pn]; e < a.rowptr[pn + 1]; ++e) corr = fma(a.vals[e], a.x[a.cols[e]], corr);
       const double layer = (pot[0] + near[0]) / FOUR_PI + corr;
-      a.y[pn] = a.alpha * a.x[pn] + a.beta * layer;
+      const double v = a.alpha * a.x[pn] + a.beta * layer;
+      if (a.ysorted) a.ysorted[ti - a.tbody_a] = v;
+      else a.y[pn] = v;
     } else {
       const double xt[3] = {tx, ty, tz};
       double u[3];
@@ -159,8 +163,11 @@ __global__ void __launch_bounds__(128) k_epilogue(TreeDev T, EpiArgs a) {
         for (int r = 0; r < 3; ++r)
           corr[r] = fma(blk[3 * r], xs[0], fma(blk[3 * r + 1], xs[1], fma(blk[3 * r + 2], xs[2], corr[r])));
       }
-      for (int r = 0; r < 3; ++r)
-        a.y[3 * pn + r] = a.alpha * a.x[3 * pn + r] + a.beta * (u[r] + corr[r]);
+      for (int r = 0; r < 3; ++r) {
+        const double v = a.alpha * a.x[3 * pn + r] + a.beta * (u[r] + corr[r]);
+        if (a.ysorted) a.ysorted[3 * (ti - a.tbody_a) + r] = v;
+        else a.y[3 * pn + r] = v;
+      }
     }
   }
 }
@@ -175,10 +182,10 @@ void launch_density(BemOp& op, const double* x, cudaStream_t s) {
 }
 
 template <int KIND>
-void launch_epilogue(BemOp& op, const EpiArgs& a, bool far, cudaStream_t s) {
+void launch_epilogue(BemOp& op, const EpiArgs& a, bool far, cudaStream_t s, int nl) {
   constexpr int C = EpiTraits<KIND>::C;
   const size_t smem = far ? (size_t)C * hcount(a.p) * sizeof(double2) : 0;
-  const int nl = op.plan.tgt.n_leaves;
+  if (nl <= 0) return;
   if (far) {
     FMM_CUDA(cudaFuncSetAttribute(k_epilogue<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(C * hcount(P_MAX) * sizeof(double2))));
@@ -320,8 +327,10 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   FMM_CUDA(cudaStreamSynchronize(s));
 }
 
-void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s) {
+void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   Plan& pl = op.plan;
+  ShardWork& sw = op.shard;
+  sharded = sharded && sw.active && !c.dense;
   const int C = layer_channels(c.kind);
   const TreeDev S = tree_dev(pl.src), T = tree_dev(pl.tgt);
   record(op, ST_TOTAL, false, s);
@@ -340,6 +349,9 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s) {
   if (c.dense)
     launch_p2p((P2PKind)c.kind, S, T, op.dense_items.get(), (int)op.dense_items_h.size(),
                op.dense_src.get(), op.dense_max_sources, w, op.part_dense.get(), op.s_near);
+  else if (sharded)
+    launch_p2p((P2PKind)c.kind, S, T, sw.items.get(), (int)sw.items_h.size(), pl.p2p_src.get(),
+               sw.max_item_sources, w, op.part.get(), op.s_near);
   else
     launch_p2p((P2PKind)c.kind, S, T, pl.d_items.get(), (int)pl.items.size(), pl.p2p_src.get(),
                op.max_item_sources, w, op.part.get(), op.s_near);
@@ -350,24 +362,38 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s) {
     const double* q = (c.kind == K_LAP_SINGLE || c.kind == K_STOKESLET) ? op.q.get() : nullptr;
     const double* d = (c.kind == K_LAP_DOUBLE || c.kind == K_STRESSLET) ? op.dip.get() : nullptr;
     record(op, ST_UP, false, s);
+    const bool own_only = sharded && !sw.virtual_mode;  // P2M of own leaves, then all-gather
+    const int* lv = own_only ? sw.p2m_leaves.get() : pl.src.leaves.get();
+    const int nlv = own_only ? sw.n_p2m_leaves : pl.src.n_leaves;
     if (c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p)
-      launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s);
+      launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, lv, nlv);
     else
-      launch_p2m(S, pl.src.leaves.get(), pl.src.n_leaves, c.p, C, q, d, op.M.get(), s);
+      launch_p2m(S, lv, nlv, c.p, C, q, d, op.M.get(), s);
+    if (own_only) shard_exchange_multipoles(op, C, c.p, s);
     launch_m2m(pl.src, pl.m2m_level_off, pl.m2m_cells.get(), c.p, C, pl.rshift_src.get(), op.M.get(), s);
     record(op, ST_UP, true, s);
     record(op, ST_M2L, false, s);
-    launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
+    if (sharded)
+      launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s, sw.gitems.get(),
+                 (int)sw.gitems_h.size(), sw.gather_cells.get(), sw.n_gather_cells, sw.gpair.get());
+    else
+      launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);
     record(op, ST_DOWN, false, s);
-    launch_l2l(pl.tgt, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
+    if (sharded)
+      launch_l2l(pl.tgt, sw.l2l_off, sw.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
+    else
+      launch_l2l(pl.tgt, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
     record(op, ST_DOWN, true, s);
   }
   FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
   EpiArgs a;
-  a.leaves = pl.tgt.leaves.get();
-  a.item_begin = c.dense ? op.dense_item_begin.get() : pl.tleaf_item_begin.get();
-  a.items = c.dense ? op.dense_items.get() : pl.d_items.get();
+  a.leaves = sharded ? sw.epi_leaves.get() : pl.tgt.leaves.get();
+  a.item_begin = c.dense ? op.dense_item_begin.get() : sharded ? sw.item_begin.get() : pl.tleaf_item_begin.get();
+  a.items = c.dense ? op.dense_items.get() : sharded ? sw.items.get() : pl.d_items.get();
+  a.ysorted = (sharded && !sw.virtual_mode) ? sw.ysend.get() : nullptr;
+  a.tbody_a = sw.tbody_a;
+  const int n_epi = sharded ? sw.n_epi_leaves : pl.tgt.n_leaves;
   a.part = c.dense ? op.part_dense.get() : op.part.get();
   a.L = op.L.get();
   a.p = c.p;
@@ -380,11 +406,12 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s) {
   a.y = c.y;
   record(op, ST_EPI, false, s);
   switch (c.kind) {
-    case K_LAP_SINGLE: launch_epilogue<K_LAP_SINGLE>(op, a, !c.dense, s); break;
-    case K_LAP_DOUBLE: launch_epilogue<K_LAP_DOUBLE>(op, a, !c.dense, s); break;
-    case K_STOKESLET: launch_epilogue<K_STOKESLET>(op, a, !c.dense, s); break;
-    default: launch_epilogue<K_STRESSLET>(op, a, !c.dense, s); break;
+    case K_LAP_SINGLE: launch_epilogue<K_LAP_SINGLE>(op, a, !c.dense, s, n_epi); break;
+    case K_LAP_DOUBLE: launch_epilogue<K_LAP_DOUBLE>(op, a, !c.dense, s, n_epi); break;
+    case K_STOKESLET: launch_epilogue<K_STOKESLET>(op, a, !c.dense, s, n_epi); break;
+    default: launch_epilogue<K_STRESSLET>(op, a, !c.dense, s, n_epi); break;
   }
+  if (a.ysorted) shard_exchange_y(op, c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE ? 1 : 3, c.y, s);
   record(op, ST_EPI, true, s);
   record(op, ST_TOTAL, true, s);
 }
@@ -423,7 +450,8 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
   prepare(op, c.kind, p, false);
   cudaStream_t s = op.s_main;
   FMM_CUDA(cudaMemcpyAsync(op.x_in.get(), x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  if (op.use_graphs) {
+  const bool sharded = op.shard.active;
+  if (op.use_graphs && !(sharded && !op.shard.virtual_mode)) {
     // captured graphs bake in buffer addresses: any reallocation invalidates them
     const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
@@ -439,7 +467,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
       cudaGraph_t g;
       FMM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       try {
-        op_layer(op, c, s);
+        op_layer(op, c, s, sharded);
       } catch (...) {
         cudaStreamEndCapture(s, &g);
         throw;
@@ -465,7 +493,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     op.kernel_launches += op.graph_kernels[key];
     op.applies += 1;
   } else {
-    op_layer(op, c, s);
+    op_layer(op, c, s, sharded);
   }
   FMM_CUDA(cudaMemcpyAsync(y, op.y_out.get(), op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }

@@ -21,6 +21,37 @@ struct Correction {
 // stage timers captured with the apply (CUDA events on the launching streams)
 enum Stage : int { ST_P2P = 0, ST_UP = 1, ST_M2L = 2, ST_DOWN = 3, ST_EPI = 4, ST_TOTAL = 5, N_STAGES = 6 };
 
+// One rank's share of a partitioned apply (shard.cu): target leaves
+// [tleaf_a, tleaf_b) and source leaves [sleaf_a, sleaf_b) in body order.
+struct ShardWork {
+  bool active = false;
+  bool virtual_mode = false;  // no collectives: full upward pass, own y entries only (tests)
+  int rank = 0, world = 1;
+  int tleaf_a = 0, tleaf_b = 0, tbody_a = 0, tbody_b = 0, max_tbody = 0;
+  int sleaf_a = 0, sleaf_b = 0, max_sleaves = 0;
+  DevBuf<int> epi_leaves;  // own target leaves (cell ids)
+  int n_epi_leaves = 0;
+  std::vector<P2PItem> items_h;
+  DevBuf<P2PItem> items;
+  DevBuf<int> item_begin;
+  int64_t part_len = 0;
+  int max_item_sources = 0;
+  std::vector<int4> gitems_h;
+  DevBuf<int4> gitems;
+  DevBuf<int> gpair;
+  DevBuf<int> gather_cells;
+  int n_gather_cells = 0;
+  std::vector<int> l2l_off;
+  DevBuf<int> l2l_cells;
+  DevBuf<int> p2m_leaves;
+  int n_p2m_leaves = 0;
+  DevBuf<int> leaf_owner_off;   // world + 1 source-leaf bounds
+  DevBuf<int> body_owner_off;   // world + 1 target-body bounds
+  DevBuf<double2> mleaf_send, mleaf_recv;
+  DevBuf<double> ysend, yrecv;
+  void* comm = nullptr;
+};
+
 struct BemOp {
   int formulation = LAPLACE_SECOND;
   double mu = 1e-3;
@@ -56,6 +87,8 @@ struct BemOp {
   DevBuf<int> dense_src, dense_item_begin;
   int64_t dense_part_len = 0;
   int dense_max_sources = 0;
+
+  ShardWork shard;
 
   // precomputed P2M basis of the system kernel ([hidx][sorted source], p2m_basis.cu)
   int basis_kind_for_sys = -1;
@@ -103,14 +136,15 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t n_panels, const do
              const double* normals, const double* areas, const double* leg_x, const double* leg_w,
              int n_gauss_singular, int formulation, double theta, int n_crit, double mu,
              double near_factor, int max_depth);
-void op_layer(BemOp& op, const LayerCall& call, cudaStream_t s);
+void op_layer(BemOp& op, const LayerCall& call, cudaStream_t s, bool sharded = false);
 void op_apply_device(BemOp& op, const double* x, double* y, int p);  // async on op.s_main
 void op_collect_stage_times(BemOp& op);  // after a sync of op.s_main
 void op_dense_apply_device(BemOp& op, const double* x, double* y);
 void op_rhs_device(BemOp& op, const double* data, double* b, int p, bool dense);
 void build_near_pairs(BemOp& op, cudaStream_t s);
 bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s);  // false: over the memory budget
-void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cudaStream_t s);
+void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cudaStream_t s,
+                      const int* leaves = nullptr, int n_leaves = -1);
 void build_correction(BemOp& op, int kind, Correction& out, cudaStream_t s);
 
 struct GmresResult {
@@ -118,6 +152,15 @@ struct GmresResult {
   std::vector<int> orders;
   bool converged = false;
 };
+// sharding (shard.cu)
+void op_shard_setup(BemOp& op, int rank, int world, const int* tleaf_bounds,
+                    const int* sleaf_bounds, const unsigned char* nccl_id);
+void op_shard_release(BemOp& op);
+void op_leaf_work(const BemOp& op, int which, double* w);
+void shard_exchange_multipoles(BemOp& op, int C, int p, cudaStream_t s);
+void shard_exchange_y(BemOp& op, int nc, double* y, cudaStream_t s);
+void nccl_unique_id(unsigned char* out);
+
 GmresResult op_gmres(BemOp& op, const double* b_dev, double tol, int p_initial, int p_min,
                      bool relaxed, int max_iter, double* x_dev);
 

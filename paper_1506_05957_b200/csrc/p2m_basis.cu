@@ -134,17 +134,22 @@ bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s) {
   return true;
 }
 
-void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cudaStream_t s) {
+void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cudaStream_t s,
+                      const int* leaves, int n_leaves) {
   const Tree& S = op.plan.src;
   const int H = hcount(p);
-  if (!S.n_leaves) return;
+  if (!leaves) {
+    leaves = S.leaves.get();
+    n_leaves = S.n_leaves;
+  }
+  if (n_leaves <= 0) return;
   if (C == 1)
-    k_p2m_basis<1><<<S.n_leaves, 256, 0, s>>>(S.leaves.get(), S.body_start.get(), S.body_count.get(),
+    k_p2m_basis<1><<<n_leaves, 256, 0, s>>>(leaves, S.body_start.get(), S.body_count.get(),
                                               S.n_points, H, op.basis_kind_for_sys,
                                               op.p2m_basis.get(), op.s_panel.get(), x, S.px.get(),
                                               S.py.get(), S.pz.get(), M);
   else
-    k_p2m_basis<4><<<S.n_leaves, 256, 0, s>>>(S.leaves.get(), S.body_start.get(), S.body_count.get(),
+    k_p2m_basis<4><<<n_leaves, 256, 0, s>>>(leaves, S.body_start.get(), S.body_count.get(),
                                               S.n_points, H, op.basis_kind_for_sys,
                                               op.p2m_basis.get(), op.s_panel.get(), x, S.px.get(),
                                               S.py.get(), S.pz.get(), M);

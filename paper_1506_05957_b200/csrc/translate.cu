@@ -509,15 +509,23 @@ k_m2l_grouped(const int4* __restrict__ items, const int* __restrict__ gpair,
   }
 }
 
-// L[cell] = sum over the cell's M2L pairs (CSR order) of their results
-__global__ void k_m2l_gather(int n_cells, const int* __restrict__ row, int CH,
-                             const double2* __restrict__ pout, double2* __restrict__ L) {
-  const int cell = blockIdx.x;
+// L[cell] = sum over the cell's M2L pairs (CSR order) of their results: 64
+// coefficients x 4 pair slices per CTA, slices added in a fixed order
+__global__ void __launch_bounds__(256)
+k_m2l_gather(const int* __restrict__ cells, const int* __restrict__ row, int CH,
+             const double2* __restrict__ pout, double2* __restrict__ L) {
+  __shared__ double2 red[4][64];
+  const int cell = cells ? cells[blockIdx.x] : blockIdx.x;
+  const int t = blockIdx.y * 64 + (threadIdx.x & 63), q = threadIdx.x >> 6;
   const int i0 = row[cell], i1 = row[cell + 1];
-  for (int t = threadIdx.x; t < CH; t += blockDim.x) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int i = i0; i < i1; ++i) s = cadd(s, pout[(size_t)i * CH + t]);
-    L[(size_t)cell * CH + t] = s;
+  double2 s = make_double2(0.0, 0.0);
+  if (t < CH)
+    for (int i = i0 + q; i < i1; i += 4) s = cadd(s, pout[(size_t)i * CH + t]);
+  red[q][threadIdx.x & 63] = s;
+  __syncthreads();
+  if (q == 0 && t < CH) {
+    const int l = threadIdx.x;
+    L[(size_t)cell * CH + t] = cadd(cadd(red[0][l], red[1][l]), cadd(red[2][l], red[3][l]));
   }
 }
 
@@ -529,9 +537,9 @@ size_t m2lg_smem() {
 }
 
 template <int P>
-void m2lg_launch(const Plan& plan, int C, const double2* M, double2* pout, cudaStream_t st) {
-  const int n = (int)plan.m2l_gitems.size();
-  if (!n) return;
+void m2lg_launch(const Plan& plan, const int4* gitems, const int* gpair, int n, int C,
+                 const double2* M, double2* pout, cudaStream_t st) {
+  if (n <= 0) return;
   const int stride = tab_size(2 * plan.igrid_p);
   for (int cb = 0; cb < C;) {
     const int rem = C - cb;
@@ -543,7 +551,7 @@ void m2lg_launch(const Plan& plan, int C, const double2* M, double2* pout, cudaS
         a4 = true;
       }
       k_m2l_grouped<P, 4><<<n, TR_WARPS * 32, m2lg_smem<P, 4>(), st>>>(
-          plan.d_m2l_gitems.get(), plan.m2l_gpair.get(), plan.m2l_src.get(), plan.igrid.get(), stride,
+          gitems, gpair, plan.m2l_src.get(), plan.igrid.get(), stride,
           M, C, cb, pout);
       cb += 4;
     } else if (rem >= 2) {
@@ -554,7 +562,7 @@ void m2lg_launch(const Plan& plan, int C, const double2* M, double2* pout, cudaS
         a2 = true;
       }
       k_m2l_grouped<P, 2><<<n, TR_WARPS * 32, m2lg_smem<P, 2>(), st>>>(
-          plan.d_m2l_gitems.get(), plan.m2l_gpair.get(), plan.m2l_src.get(), plan.igrid.get(), stride,
+          gitems, gpair, plan.m2l_src.get(), plan.igrid.get(), stride,
           M, C, cb, pout);
       cb += 2;
     } else {
@@ -565,7 +573,7 @@ void m2lg_launch(const Plan& plan, int C, const double2* M, double2* pout, cudaS
         a1 = true;
       }
       k_m2l_grouped<P, 1><<<n, TR_WARPS * 32, m2lg_smem<P, 1>(), st>>>(
-          plan.d_m2l_gitems.get(), plan.m2l_gpair.get(), plan.m2l_src.get(), plan.igrid.get(), stride,
+          gitems, gpair, plan.m2l_src.get(), plan.igrid.get(), stride,
           M, C, cb, pout);
       cb += 1;
     }
@@ -575,18 +583,28 @@ void m2lg_launch(const Plan& plan, int C, const double2* M, double2* pout, cudaS
 
 // ------------------------------------------------------------------ launchers
 void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
-                cudaStream_t st) {
+                cudaStream_t st, const int4* gitems, int n_gitems, const int* cells, int n_cells,
+                const int* gpair) {
+  if (!gpair) gpair = plan.m2l_gpair.get();
   // part holds one result block per M2L pair (CSR order): n_m2l * C * hcount(p)
+  if (!gitems) {
+    gitems = plan.d_m2l_gitems.get();
+    n_gitems = (int)plan.m2l_gitems.size();
+  }
+  if (n_cells < 0) n_cells = plan.tgt.n_cells;
   switch (p) {
-#define G_CASE(PP) case PP: m2lg_launch<PP>(plan, C, M, part, st); break;
+#define G_CASE(PP) case PP: m2lg_launch<PP>(plan, gitems, gpair, n_gitems, C, M, part, st); break;
     G_CASE(0) G_CASE(1) G_CASE(2) G_CASE(3) G_CASE(4) G_CASE(5) G_CASE(6)
     G_CASE(7) G_CASE(8) G_CASE(9) G_CASE(10) G_CASE(11) G_CASE(12) G_CASE(13)
     G_CASE(14) G_CASE(15) G_CASE(16) G_CASE(17) G_CASE(18) G_CASE(19) G_CASE(20)
 #undef G_CASE
     default: throw ArgumentError("M2L: expansion order out of range");
   }
-  k_m2l_gather<<<plan.tgt.n_cells, 128, 0, st>>>(plan.tgt.n_cells, plan.m2l_row.get(), C * hcount(p),
-                                                 part, L);
+  if (n_cells > 0) {
+    const int CH = C * hcount(p);
+    dim3 grid(n_cells, (CH + 63) / 64);
+    k_m2l_gather<<<grid, 256, 0, st>>>(cells, plan.m2l_row.get(), CH, part, L);
+  }
   FMM_LAUNCH_CHECK();
 }
 

@@ -333,6 +333,43 @@ class GpuBemOperator:
     def set_timing(self, enable: bool, use_graphs: bool = True):
         N.check(self._lib.fmmbem_op_set_timing(self._h, 1 if enable else 0, 1 if use_graphs else 0))
 
+    # -- multi-GPU ---------------------------------------------------------------
+    def leaf_work(self, which: str = "tgt") -> np.ndarray:
+        """Per-leaf work weights (body order) used to partition the leaves across ranks."""
+        w = np.zeros(self.plan.n_tgt_leaves if which == "tgt" else self.plan.n_src_leaves)
+        N.check(self._lib.fmmbem_op_leaf_work(self._h, 0 if which == "tgt" else 1, N.dptr(w)))
+        return w
+
+    def shard(self, rank: int, world: int, tleaf_bounds, sleaf_bounds, nccl_id: bytes | None = None):
+        """Own target leaves [tb[rank], tb[rank+1]) and source leaves [sb[rank], sb[rank+1]).
+
+        nccl_id: 128 bytes shared by all ranks (``nccl_unique_id()`` on rank 0); None makes a
+        "virtual" shard that computes only its own rows without collectives (testing).
+        """
+        tb = np.ascontiguousarray(tleaf_bounds, dtype=np.int32)
+        sb = np.ascontiguousarray(sleaf_bounds, dtype=np.int32)
+        if tb.shape != (world + 1,) or sb.shape != (world + 1,):
+            raise ValueError("bounds must have world + 1 entries")
+        if nccl_id is not None and len(nccl_id) != 128:
+            raise ValueError("nccl_id must be 128 bytes")
+        N.check(self._lib.fmmbem_op_shard(self._h, int(rank), int(world), N.i32ptr(tb), N.i32ptr(sb),
+                                          nccl_id))
+
+    def unshard(self):
+        N.check(self._lib.fmmbem_op_unshard(self._h))
+
+    def owned_panels(self, tleaf_bounds, rank: int) -> np.ndarray:
+        """Panel indices whose rows rank `rank` computes under the given target split."""
+        t = self.plan.tree("tgt")
+        leaves = np.flatnonzero(t["is_leaf"])
+        leaves = leaves[np.argsort(t["body_start"][leaves], kind="stable")]
+        a, b = int(tleaf_bounds[rank]), int(tleaf_bounds[rank + 1])
+        if a == b:
+            return np.zeros(0, dtype=np.int64)
+        s0 = t["body_start"][leaves[a]]
+        s1 = t["body_start"][leaves[b - 1]] + t["body_count"][leaves[b - 1]]
+        return np.sort(t["perm"][s0:s1])
+
     def counters(self):
         """(kernel launches so far, graph applies so far, last GMRES call device ms)."""
         kl = ctypes.c_int64(0)

@@ -36,6 +36,42 @@ def partition_contiguous(weights, world: int) -> np.ndarray:
     return b
 
 
+def leaf_bounds(op, world: int):
+    """(target, source) leaf bounds for `world` ranks from the operator's work weights."""
+    return (partition_contiguous(op.leaf_work("tgt"), world),
+            partition_contiguous(op.leaf_work("src"), world))
+
+
+def nccl_unique_id() -> bytes:
+    import ctypes
+
+    from . import _native as N
+
+    buf = ctypes.create_string_buffer(128)
+    N.check(N.load().fmmbem_nccl_unique_id(buf))
+    return buf.raw
+
+
+def broadcast_bytes(data: bytes | None, src: int = 0) -> bytes:
+    """Share a small byte string from rank `src` (torch.distributed object broadcast)."""
+    import torch.distributed as dist
+
+    obj = [data]
+    dist.broadcast_object_list(obj, src=src)
+    return obj[0]
+
+
+def shard_operator(op, rank: int, world: int):
+    """Partition op's work over the torch.distributed world (one GPU per rank).
+
+    Every rank computes the same bounds; rank 0 creates the NCCL id and shares it.
+    """
+    tb, sb = leaf_bounds(op, world)
+    uid = broadcast_bytes(nccl_unique_id() if rank == 0 else None)
+    op.shard(rank, world, tb, sb, uid)
+    return tb, sb
+
+
 def reduce_timing(local_ms: float, local_count: float, device=None):
     """(max over ranks of the device time, sum over ranks of the work units).
 

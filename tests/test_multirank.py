@@ -64,3 +64,34 @@ def test_partition_covers_in_order(world):
 
 def test_single_process_reduction_is_identity():
     assert reduce_timing(3.0, 2) == (3.0, 2.0)
+
+
+def _bytes_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_1506_05957_b200.parallel import broadcast_bytes
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        got = broadcast_bytes(bytes(range(128)) if rank == 0 else None)
+        out.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_nccl_id_broadcast():
+    """The shard setup shares rank 0's 128-byte NCCL id with every rank."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bytes_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[1] == bytes(range(128)) for r in res)
