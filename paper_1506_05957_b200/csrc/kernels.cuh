@@ -36,6 +36,9 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
                 cudaStream_t st, const int4* gitems = nullptr, int n_gitems = -1,
                 const int* cells = nullptr, int n_cells = -1, const int* gpair = nullptr);
 void compute_igrid_full(const double* d_off, int n_off, int order, double2* out, cudaStream_t s);
+// M2M through octant-grouped child translations (cout: per-cell child contributions)
+void launch_m2m_grouped(const Plan& plan, int p, int C, const double2* rfull, double2* M,
+                        double2* cout, cudaStream_t st);
 // L2L into the cells listed per level whose parent has a nonzero local expansion
 void launch_l2l(const Tree& T, const std::vector<int>& level_off, const int* cells, int p, int C,
                 const double2* rfull, double2* L, cudaStream_t st);

@@ -236,6 +236,7 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
   } else {
     op.part.ensure((size_t)std::max<int64_t>(op.plan.part_len, 1) * 3);
     op.M.ensure((size_t)op.plan.src.n_cells * C * hcount(p));
+    op.m2m_cout.ensure((size_t)op.plan.src.n_cells * C * hcount(p));
     op.L.ensure((size_t)op.plan.tgt.n_cells * C * hcount(p));
     op.m2l_part.ensure((size_t)std::max(op.plan.n_m2l, 1) * C * hcount(p));
     plan_ensure_igrid(op.plan, p, op.s_main);
@@ -370,7 +371,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     else
       launch_p2m(S, lv, nlv, c.p, C, q, d, op.M.get(), s);
     if (own_only) shard_exchange_multipoles(op, C, c.p, s);
-    launch_m2m(pl.src, pl.m2m_level_off, pl.m2m_cells.get(), c.p, C, pl.rshift_src.get(), op.M.get(), s);
+    launch_m2m_grouped(pl, c.p, C, pl.rshift_src.get(), op.M.get(), op.m2m_cout.get(), s);
     record(op, ST_UP, true, s);
     record(op, ST_M2L, false, s);
     if (sharded)
@@ -456,7 +457,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
                                           op.x_in.get(), op.y_out.get(), op.m2l_part.get(),
-                                          op.p2m_basis.get()};
+                                          op.p2m_basis.get(), op.m2m_cout.get()};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;

@@ -78,7 +78,7 @@ struct BemOp {
 
   // work buffers
   DevBuf<double> x_in, y_out, q, dip, wsrc, part, part_dense, stage_x, stage_y;
-  DevBuf<double2> M, L, m2l_part;
+  DevBuf<double2> M, L, m2l_part, m2m_cout;
   int max_item_sources = 0;
   // dense (direct) P2P lists
   bool dense_ready = false;

@@ -93,6 +93,10 @@ struct Plan {
   // M2L (or an ancestor's), L2L only below cells that carry a local expansion
   std::vector<int> m2m_level_off, l2l_level_off;
   DevBuf<int> m2m_cells, l2l_cells;
+  // octant-grouped M2M: items (rtab id, begin, end) into m2m_gchild, per parent level
+  std::vector<int> m2m_gitem_off;
+  DevBuf<int4> d_m2m_gitems;
+  DevBuf<int> m2m_gchild;
 
   // M2M / L2L translation tables: R(d) for the 8 child octants of every level, up to igrid... P_MAX
   DevBuf<double2> rshift_src;  // [level][octant][(P_MAX+1)^2] full storage

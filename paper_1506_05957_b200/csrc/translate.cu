@@ -608,6 +608,198 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
   FMM_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------------------------ M2M, octant-grouped
+// Children at one level that sit in the same octant of their parents share
+// R(d): one CTA per (level, octant, <= 8 children) applies it to 4 child
+// vectors per pass (same scheme as k_m2l_grouped, with the M2M index map and
+// the j <= n, |m-k| <= n-j mask); every child's contribution goes to its own
+// slot and k_children_sum adds the children of each parent in octant order.
+template <int P, int CK>
+__global__ void __launch_bounds__(TR_WARPS * 32)
+k_m2m_grouped(const int4* __restrict__ items, const int* __restrict__ gchild,
+              const double2* __restrict__ table, int table_stride, const double2* __restrict__ M,
+              int Ctot, int cbase, double2* __restrict__ cout) {
+  constexpr int BJ = tr_bj(P);
+  constexpr int H = (P + 1) * (P + 2) / 2;
+  constexpr int S = (P + 1) * (P + 1);
+  constexpr int NV = 4;
+  constexpr int NP = NV / CK;
+  extern __shared__ double2 sh[];
+  double2* sT = sh;
+  double2* sM = sh + S;  // [NV][S]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 it = items[blockIdx.x];
+  {
+    const double2* T = table + (size_t)it.x * table_stride;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) cp_async16(sT + i, T + i);
+    cp_async_commit();
+  }
+  int oc = -1, r0 = 0;
+  {
+    int cum = 0;
+    for (int kk = 0; kk <= P; ++kk) {
+      const int nt = (P - kk + 1 + BJ - 1) / BJ;
+      if (oc < 0 && lane < cum + nt) {
+        oc = kk;
+        r0 = kk + (lane - cum) * BJ;
+      }
+      cum += nt;
+    }
+  }
+  const bool active = oc >= 0;
+  for (int e0 = it.y; e0 < it.z; e0 += NP) {
+    const int np = min(NP, it.z - e0);
+    const int nv = np * CK;
+    __syncthreads();
+    for (int f = threadIdx.x; f < NV * S; f += blockDim.x) {
+      const int v = f / S, g = f - v * S;
+      double2 val = make_double2(0.0, 0.0);
+      if (v < nv) {
+        const int ch = gchild[e0 + v / CK], c = cbase + v % CK;
+        const int n = (int)__fsqrt_rz((float)g);
+        val = hget(M + ((size_t)ch * Ctot + c) * H, n, g - n * n - n);
+      }
+      sM[f] = val;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    double2 acc[NV][BJ];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int t = 0; t < BJ; ++t) acc[v][t] = make_double2(0.0, 0.0);
+    if (active) {
+      for (int ai = warp; ai < 2 * P + 1; ai += TR_WARPS) {
+        const int am = ai - P;
+        const int b0 = am < 0 ? -am : am;
+        const int col = oc - am;
+        const int acol = col < 0 ? -col : col;
+        auto tval = [&](int row) -> double2 {  // R_{row}^{col}, zero outside the triangle
+          const int N = min(max(row, 0), P);
+          const double2 v = sT[pidx(N, max(min(col, N), -N))];
+          return row >= acol ? v : make_double2(0.0, 0.0);
+        };
+        double2 w[BJ];
+#pragma unroll
+        for (int t = 0; t < BJ; ++t) w[t] = tval(r0 + t - b0);
+        int lead = r0 - b0 - 1;
+        const double2* ip = sM + b0 * b0 + b0 + am;
+        int istep = 2 * b0 + 2;
+        auto step = [&](int q) {
+          double2 mv[NV];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) mv[v] = ip[v * S];
+          const double2 nw = tval(lead);
+          ip += istep;
+          istep += 2;
+          --lead;
+#pragma unroll
+          for (int t = 0; t < BJ; ++t)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v][t] = cfma(mv[v], w[(t + BJ - q) % BJ], acc[v][t]);
+          w[(BJ - 1 - q) % BJ] = nw;
+        };
+        int b = b0;
+        for (; b + BJ - 1 <= P; b += BJ) {
+#pragma unroll
+          for (int q = 0; q < BJ; ++q) step(q);
+        }
+#pragma unroll
+        for (int q = 0; q < BJ - 1; ++q)
+          if (b + q <= P) step(q);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      __syncthreads();
+      double2* red = sM;
+#pragma unroll
+      for (int t = 0; t < BJ; ++t) red[(warp * 32 + lane) * BJ + t] = acc[v][t];
+      __syncthreads();
+      if (warp == 0 && active && v < nv) {
+        const int ch = gchild[e0 + v / CK], c = cbase + v % CK;
+#pragma unroll
+        for (int t = 0; t < BJ; ++t) {
+          const int r = r0 + t;
+          if (r > P) continue;
+          double2 sum = red[lane * BJ + t];
+          for (int w2 = 1; w2 < TR_WARPS; ++w2) sum = cadd(sum, red[(w2 * 32 + lane) * BJ + t]);
+          cout[((size_t)ch * Ctot + c) * H + r * (r + 1) / 2 + oc] = sum;
+        }
+      }
+    }
+  }
+}
+
+// M[parent] = sum of its children's contributions in octant order
+__global__ void k_children_sum(const int* __restrict__ parents, const int* __restrict__ first_child,
+                               const int* __restrict__ n_child, int CH,
+                               const double2* __restrict__ cout, double2* __restrict__ M) {
+  const int par = parents[blockIdx.x];
+  const int f = first_child[par], nc = n_child[par];
+  for (int t = threadIdx.x; t < CH; t += blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = 0; k < nc; ++k) s = cadd(s, cout[(size_t)(f + k) * CH + t]);
+    M[(size_t)par * CH + t] = s;
+  }
+}
+
+template <int P, int CK>
+size_t m2mg_smem() {
+  constexpr int S = (P + 1) * (P + 1);
+  const size_t red = (size_t)TR_WARPS * 32 * tr_bj(P);
+  return ((size_t)S + std::max((size_t)4 * S, red)) * sizeof(double2);
+}
+
+template <int P, int CK>
+void m2mg_launch_one(const int4* items, int n, const int* gchild, const double2* rfull,
+                     const double2* M, int C, int cb, double2* cout, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    FMM_CUDA(cudaFuncSetAttribute(k_m2m_grouped<P, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)m2mg_smem<P, CK>()));
+    attr = true;
+  }
+  k_m2m_grouped<P, CK><<<n, TR_WARPS * 32, m2mg_smem<P, CK>(), st>>>(items, gchild, rfull, tab_size(P_MAX),
+                                                                     M, C, cb, cout);
+}
+
+template <int P>
+void m2mg_launch(const int4* items, int n, const int* gchild, const double2* rfull, const double2* M,
+                 int C, double2* cout, cudaStream_t st) {
+  if (n <= 0) return;
+  for (int cb = 0; cb < C;) {
+    const int rem = C - cb;
+    if (rem >= 4) { m2mg_launch_one<P, 4>(items, n, gchild, rfull, M, C, cb, cout, st); cb += 4; }
+    else if (rem >= 2) { m2mg_launch_one<P, 2>(items, n, gchild, rfull, M, C, cb, cout, st); cb += 2; }
+    else { m2mg_launch_one<P, 1>(items, n, gchild, rfull, M, C, cb, cout, st); cb += 1; }
+  }
+  FMM_LAUNCH_CHECK();
+}
+
+void launch_m2m_grouped(const Plan& plan, int p, int C, const double2* rfull, double2* M,
+                        double2* cout, cudaStream_t st) {
+  const Tree& S = plan.src;
+  const int CH = C * hcount(p);
+  for (int l = (int)plan.m2m_level_off.size() - 2; l >= 0; --l) {
+    const int np = plan.m2m_level_off[l + 1] - plan.m2m_level_off[l];
+    if (np <= 0) continue;
+    const int ia = plan.m2m_gitem_off[l], ib = plan.m2m_gitem_off[l + 1];
+    const int4* items = plan.d_m2m_gitems.get() + ia;
+    switch (p) {
+#define MG_CASE(PP) case PP: m2mg_launch<PP>(items, ib - ia, plan.m2m_gchild.get(), rfull, M, C, cout, st); break;
+      MG_CASE(0) MG_CASE(1) MG_CASE(2) MG_CASE(3) MG_CASE(4) MG_CASE(5) MG_CASE(6)
+      MG_CASE(7) MG_CASE(8) MG_CASE(9) MG_CASE(10) MG_CASE(11) MG_CASE(12) MG_CASE(13)
+      MG_CASE(14) MG_CASE(15) MG_CASE(16) MG_CASE(17) MG_CASE(18) MG_CASE(19) MG_CASE(20)
+#undef MG_CASE
+      default: throw ArgumentError("M2M: expansion order out of range");
+    }
+    k_children_sum<<<np, 128, 0, st>>>(plan.m2m_cells.get() + plan.m2m_level_off[l], S.first_child.get(),
+                                       S.n_child.get(), CH, cout, M);
+    FMM_LAUNCH_CHECK();
+  }
+}
+
 void launch_m2m(const Tree& S, const std::vector<int>& level_off, const int* cells, int p, int C,
                 const double2* rfull, double2* M, cudaStream_t st) {
   TrArgs a{};

@@ -324,6 +324,32 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
       plan.m2m_level_off.push_back((int)cells.size());
     }
     plan.m2m_cells.upload(cells.empty() ? std::vector<int>(1, 0) : cells, s);
+    // children of those parents grouped by (level, octant) -> shared R(d)
+    std::vector<int4> gitems;
+    std::vector<int> gchild;
+    plan.m2m_gitem_off.assign(1, 0);
+    for (int l = 0; l < S.n_levels; ++l) {
+      std::vector<std::vector<int>> by_oct(8);
+      for (int k = plan.m2m_level_off[l]; k < plan.m2m_level_off[l + 1]; ++k) {
+        const int par = cells[k];
+        for (int ch = S.h_first_child[par]; ch < S.h_first_child[par] + S.h_n_child[par]; ++ch) {
+          const int o = (S.h_cx[ch] > S.h_cx[par] ? 1 : 0) | (S.h_cy[ch] > S.h_cy[par] ? 2 : 0) |
+                        (S.h_cz[ch] > S.h_cz[par] ? 4 : 0);
+          by_oct[o].push_back(ch);
+        }
+      }
+      for (int o = 0; o < 8; ++o) {
+        const auto& v = by_oct[o];
+        for (size_t i = 0; i < v.size(); i += 8) {
+          const int b = (int)gchild.size();
+          for (size_t j = i; j < std::min(v.size(), i + 8); ++j) gchild.push_back(v[j]);
+          gitems.push_back(make_int4((l + 1) * 8 + o, b, (int)gchild.size(), 0));
+        }
+      }
+      plan.m2m_gitem_off.push_back((int)gitems.size());
+    }
+    plan.d_m2m_gitems.upload(gitems.empty() ? std::vector<int4>(1) : gitems, s);
+    plan.m2m_gchild.upload(gchild.empty() ? std::vector<int>(1, 0) : gchild, s);
     for (int c = 0; c < T.n_cells; ++c)
       if (plan.h_m2l_row[c + 1] > plan.h_m2l_row[c]) nz[c] = 1;
     for (int c = 1; c < T.n_cells; ++c)
