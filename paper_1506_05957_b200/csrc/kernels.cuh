@@ -36,6 +36,12 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
                 cudaStream_t st, const int4* gitems = nullptr, int n_gitems = -1,
                 const int* cells = nullptr, int n_cells = -1, const int* gpair = nullptr);
 void compute_igrid_full(const double* d_off, int n_off, int order, double2* out, cudaStream_t s);
+void compute_rot_tables(const double* d_off, int n_off, int P, double* out, double* geo,
+                        cudaStream_t s);
+size_t rot_table_size(int P);
+void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
+                    int C, const double2* M, double2* pout, cudaStream_t st);
+constexpr int M2L_ROT_MIN_P = 6;  // rotation-based M2L from this order up
 // M2M through octant-grouped child translations (cout: per-cell child contributions)
 void launch_m2m_grouped(const Plan& plan, int p, int C, const double2* rfull, double2* M,
                         double2* cout, cudaStream_t st);

@@ -240,6 +240,7 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
     op.L.ensure((size_t)op.plan.tgt.n_cells * C * hcount(p));
     op.m2l_part.ensure((size_t)std::max(op.plan.n_m2l, 1) * C * hcount(p));
     plan_ensure_igrid(op.plan, p, op.s_main);
+    if (op.plan.use_rot) plan_ensure_rot(op.plan, p, op.s_main);
     if (kind == op.basis_kind_for_sys) op.use_basis = ensure_p2m_basis(op, p, op.s_main);
   }
 }
@@ -279,8 +280,12 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   op.n_gauss_singular = n_gauss_singular;
   op.n_panels = P;
   op.n = formulation == STOKES ? 3 * P : P;
-  FMM_CUDA(cudaStreamCreateWithFlags(&op.s_main, cudaStreamNonBlocking));
-  FMM_CUDA(cudaStreamCreateWithFlags(&op.s_near, cudaStreamNonBlocking));
+  // the far-field chain (many short, dependent launches) gets the higher priority;
+  // the near field (one large, independent launch) fills the remaining SMs
+  int prio_lo = 0, prio_hi = 0;
+  FMM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  FMM_CUDA(cudaStreamCreateWithPriority(&op.s_main, cudaStreamNonBlocking, prio_hi));
+  FMM_CUDA(cudaStreamCreateWithPriority(&op.s_near, cudaStreamNonBlocking, prio_lo));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_join, cudaEventDisableTiming));
   for (auto& e : op.ev) FMM_CUDA(cudaEventCreate(&e));
@@ -457,7 +462,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
                                           op.x_in.get(), op.y_out.get(), op.m2l_part.get(),
-                                          op.p2m_basis.get(), op.m2m_cout.get()};
+                                          op.p2m_basis.get(), op.m2m_cout.get(), op.plan.rot.get()};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;
@@ -556,6 +561,7 @@ void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig
   const TreeDev S = tree_dev(plan.src), T = tree_dev(plan.tgt);
   if (parts & 1) {
     plan_ensure_igrid(plan, p, s);
+    if (plan.use_rot) plan_ensure_rot(plan, p, s);
     DevBuf<double2> M((size_t)plan.src.n_cells * C * hcount(p)), L((size_t)plan.tgt.n_cells * C * hcount(p));
     DevBuf<double2> part((size_t)std::max(plan.n_m2l, 1) * C * hcount(p));
     launch_p2m(S, plan.src.leaves.get(), plan.src.n_leaves, p, C, q_orig ? qs.get() : nullptr,

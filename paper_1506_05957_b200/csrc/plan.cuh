@@ -66,6 +66,11 @@ struct Plan {
   DevBuf<double> off_d;    // 3 * n_offsets, the (lattice-exact) translation vectors
   DevBuf<double2> igrid;   // n_offsets * (2 igrid_p + 1)^2, FULL flat storage n^2+n+m
   int igrid_p = -1;        // I tables hold orders up to 2 * igrid_p
+  // rotation-based M2L (m2l_rot.cu): per offset the scaled Wigner matrices a^n, n <= rot_p,
+  // and (|D|, theta, phi)
+  DevBuf<double> rot, rot_geo;
+  int rot_p = -1;
+  bool use_rot = true;  // FMMBEM_DENSE_M2L=1 selects the dense contraction instead
   // M2L work items: (target cell, pair begin, pair end, item id), <= 16 pairs each
   std::vector<int4> m2l_items;
   DevBuf<int4> d_m2l_items;
@@ -108,6 +113,7 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
                 int n_crit, double theta, int max_depth, cudaStream_t s);
 // (re)build the irregular-harmonic tables for M2L up to order 2p
 void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s);
+void plan_ensure_rot(Plan& plan, int p, cudaStream_t s);
 // dense "every source leaf for every target leaf" item list (dense_apply)
 void plan_dense_items(const Plan& plan, std::vector<P2PItem>& items, std::vector<int>& row,
                       std::vector<int>& src, std::vector<int>& item_begin, int64_t& part_len);

@@ -592,7 +592,9 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
     n_gitems = (int)plan.m2l_gitems.size();
   }
   if (n_cells < 0) n_cells = plan.tgt.n_cells;
-  switch (p) {
+  if (plan.use_rot && p >= M2L_ROT_MIN_P && plan.rot_p >= p) {
+    launch_m2l_rot(plan, gitems, gpair, n_gitems, p, C, M, part, st);
+  } else switch (p) {
 #define G_CASE(PP) case PP: m2lg_launch<PP>(plan, gitems, gpair, n_gitems, C, M, part, st); break;
     G_CASE(0) G_CASE(1) G_CASE(2) G_CASE(3) G_CASE(4) G_CASE(5) G_CASE(6)
     G_CASE(7) G_CASE(8) G_CASE(9) G_CASE(10) G_CASE(11) G_CASE(12) G_CASE(13)

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <tuple>
 
@@ -196,6 +197,16 @@ void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s) {
   plan.igrid_p = p;
 }
 
+void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
+  FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
+  if (plan.rot_p >= p) return;
+  plan.rot.resize((size_t)std::max(plan.n_offsets, 1) * rot_table_size(p));
+  plan.rot_geo.resize((size_t)std::max(plan.n_offsets, 1) * 3);
+  compute_rot_tables(plan.off_d.get(), plan.n_offsets, p, plan.rot.get(), plan.rot_geo.get(), s);
+  FMM_CUDA(cudaStreamSynchronize(s));
+  plan.rot_p = p;
+}
+
 void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt_xyz, int64_t nt,
                 int n_crit, double theta, int max_depth, cudaStream_t s) {
   FMM_REQUIRE(ns > 0 && nt > 0, "points must be nonempty (N, 3) arrays");
@@ -205,6 +216,7 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
   FMM_REQUIRE(max_depth >= 1 && max_depth <= MAX_DEPTH_LIMIT, "max_depth must be in [1, 21]");
   plan.n_crit = n_crit;
   plan.theta = theta;
+  plan.use_rot = std::getenv("FMMBEM_DENSE_M2L") == nullptr;
   plan.max_depth = max_depth;
   plan.recip.upload(make_recip_table(), s);
   build_trees(plan, src_xyz, ns, tgt_xyz, nt, s);
