@@ -616,8 +616,10 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
 // vectors per pass (same scheme as k_m2l_grouped, with the M2M index map and
 // the j <= n, |m-k| <= n-j mask); every child's contribution goes to its own
 // slot and k_children_sum adds the children of each parent in octant order.
+constexpr int M2M_WARPS = 8;  // warps splitting the input orders of one M2M item
+
 template <int P, int CK>
-__global__ void __launch_bounds__(TR_WARPS * 32)
+__global__ void __launch_bounds__(M2M_WARPS * 32)
 k_m2m_grouped(const int4* __restrict__ items, const int* __restrict__ gchild,
               const double2* __restrict__ table, int table_stride, const double2* __restrict__ M,
               int Ctot, int cbase, double2* __restrict__ cout) {
@@ -671,7 +673,7 @@ k_m2m_grouped(const int4* __restrict__ items, const int* __restrict__ gchild,
 #pragma unroll
       for (int t = 0; t < BJ; ++t) acc[v][t] = make_double2(0.0, 0.0);
     if (active) {
-      for (int ai = warp; ai < 2 * P + 1; ai += TR_WARPS) {
+      for (int ai = warp; ai < 2 * P + 1; ai += M2M_WARPS) {
         const int am = ai - P;
         const int b0 = am < 0 ? -am : am;
         const int col = oc - am;
@@ -725,7 +727,7 @@ k_m2m_grouped(const int4* __restrict__ items, const int* __restrict__ gchild,
           const int r = r0 + t;
           if (r > P) continue;
           double2 sum = red[lane * BJ + t];
-          for (int w2 = 1; w2 < TR_WARPS; ++w2) sum = cadd(sum, red[(w2 * 32 + lane) * BJ + t]);
+          for (int w2 = 1; w2 < M2M_WARPS; ++w2) sum = cadd(sum, red[(w2 * 32 + lane) * BJ + t]);
           cout[((size_t)ch * Ctot + c) * H + r * (r + 1) / 2 + oc] = sum;
         }
       }
@@ -749,7 +751,7 @@ __global__ void k_children_sum(const int* __restrict__ parents, const int* __res
 template <int P, int CK>
 size_t m2mg_smem() {
   constexpr int S = (P + 1) * (P + 1);
-  const size_t red = (size_t)TR_WARPS * 32 * tr_bj(P);
+  const size_t red = (size_t)M2M_WARPS * 32 * tr_bj(P);
   return ((size_t)S + std::max((size_t)4 * S, red)) * sizeof(double2);
 }
 
@@ -762,7 +764,7 @@ void m2mg_launch_one(const int4* items, int n, const int* gchild, const double2*
                                   (int)m2mg_smem<P, CK>()));
     attr = true;
   }
-  k_m2m_grouped<P, CK><<<n, TR_WARPS * 32, m2mg_smem<P, CK>(), st>>>(items, gchild, rfull, tab_size(P_MAX),
+  k_m2m_grouped<P, CK><<<n, M2M_WARPS * 32, m2mg_smem<P, CK>(), st>>>(items, gchild, rfull, tab_size(P_MAX),
                                                                      M, C, cb, cout);
 }
 

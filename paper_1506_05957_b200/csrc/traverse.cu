@@ -352,9 +352,9 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
       }
       for (int o = 0; o < 8; ++o) {
         const auto& v = by_oct[o];
-        for (size_t i = 0; i < v.size(); i += 8) {
+        for (size_t i = 0; i < v.size(); i += 4) {  // one 4-vector pass per CTA
           const int b = (int)gchild.size();
-          for (size_t j = i; j < std::min(v.size(), i + 8); ++j) gchild.push_back(v[j]);
+          for (size_t j = i; j < std::min(v.size(), i + 4); ++j) gchild.push_back(v[j]);
           gitems.push_back(make_int4((l + 1) * 8 + o, b, (int)gchild.size(), 0));
         }
       }
