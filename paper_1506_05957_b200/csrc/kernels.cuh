@@ -39,6 +39,10 @@ void compute_igrid_full(const double* d_off, int n_off, int order, double2* out,
 void compute_rot_tables(const double* d_off, int n_off, int P, double* out, double* geo,
                         cudaStream_t s);
 size_t rot_table_size(int P);
+size_t rot_frag_size(int P);
+inline size_t rot_aux_size(int P) { return (size_t)(4 * P + 4); }
+void build_rot_aux(const double* geo, int n_off, int P, double* aux, cudaStream_t s);
+void build_rot_frag(const double* rot, int n_off, int P, double* out, cudaStream_t s);
 void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
                     int C, const double2* M, double2* pout, cudaStream_t st);
 constexpr int M2L_ROT_MIN_P = 6;  // rotation-based M2L from this order up

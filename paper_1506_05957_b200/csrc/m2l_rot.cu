@@ -19,6 +19,8 @@
 // (offset, <= 8 pairs) stages them in shared memory and runs the three stages
 // for up to 8 vectors (pairs x channels) at once; results go to the per-pair
 // slots that k_m2l_gather adds per target cell in a fixed order.
+#include <utility>
+
 #include "kernels.cuh"
 
 namespace fmmbem {
@@ -90,140 +92,297 @@ __global__ void k_rot_tables(const double* __restrict__ off, int n_off, int P, d
   }
 }
 
-constexpr int ROT_THREADS = 256;
-constexpr int ROT_V = 8;  // vectors (pairs x channels) per pass
+// ---- FP64 tensor-core (DMMA m8n8k4) formulation -------------------------
+//
+// With the real-field symmetries M_n^{-k} = (-1)^k conj(M_n^k) (also for the
+// phased M, M' and L'), each stage splits into two real products of order
+// (n+1) x (n+1), one on the real parts and one on the imaginary parts:
+//   A:  Re M'_n^m = sum_{k>=0} SA_re[m][k] Re Mf_n^k,   SA_re = a_{m,k} + (-1)^k a_{m,-k} (k>0)
+//       Im M'_n^m = sum_{k>=0} SA_im[m][k] Im Mf_n^k,   SA_im = a_{m,k} - (-1)^k a_{m,-k}
+//   B:  L'_j^k    = (-1)^(j+k) sum_{n>=k} z_{n+j} conj(M'_n^k)            (Hankel in z)
+//   C:  Re L~_j^k = sum_{l>=0} SC_re[k][l] Re L'_j^l,   SC_re = a_{l,k} + (-1)^l a_{-l,k}
+//       Im L~_j^k = sum_{l>=0} SC_im[k][l] Im L'_j^l,   L_j^k = e^{-ik phi} L~_j^k
+// A warp takes 8 vectors (pairs x channels) of one offset; the vectors are
+// the n = 8 columns of mma.sync.m8n8k4.f64, the real matrices SA/SC the row
+// operand (pre-swizzled per 8x4 tile into lane order at setup, so a fragment
+// is one coalesced 256-byte load), stage B's Hankel operand is formed from z.
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+__host__ __device__ constexpr int frag_mt(int n) { return (n + 8) >> 3; }
+__host__ __device__ constexpr int frag_ks(int n) { return (n + 4) >> 2; }
+__host__ __device__ constexpr int aux_stride(int P) { return 4 * P + 4; }
+__host__ __device__ constexpr int frag_base(int n) {  // tiles of degrees < n
+  int b = 0;
+  for (int i = 0; i < n; ++i) b += frag_mt(i) * frag_ks(i);
+  return b;
 }
 
-__global__ void __launch_bounds__(ROT_THREADS)
-k_m2l_rot(const int4* __restrict__ items, const int* __restrict__ gpair,
-          const int* __restrict__ pair_src, const double* __restrict__ rot, int rot_stride,
-          const double* __restrict__ geo, int p, const double2* __restrict__ M, int Ctot, int C,
+// one thread per (offset, table, tile, lane)
+__global__ void k_rot_frag(const double* __restrict__ rot, int n_off, int P, int ttot,
+                           double* __restrict__ out) {
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)n_off * 4 * ttot * 32) return;
+  const int lane = (int)(gid & 31);
+  int64_t r = gid >> 5;
+  const int t = (int)(r % ttot);
+  r /= ttot;
+  const int which = (int)(r & 3);
+  const int u = (int)(r >> 2);
+  int n = 0;
+  while (n < P && frag_base(n + 1) <= t) ++n;
+  const int lt = t - frag_base(n), ks = frag_ks(n);
+  const int row = (lt / ks) * 8 + (lane >> 2), col = (lt % ks) * 4 + (lane & 3);
+  double v = 0.0;
+  if (row <= n && col <= n) {
+    const double* a = rot + (size_t)u * rot_size(P) + rot_base(n) + n * (2 * n + 1) + n;
+    const int W = 2 * n + 1;  // a(m, k) = a[m * W + k], m, k in [-n, n]
+    if (which < 2) {  // SA: row m, col k
+      const int m = row, k = col;
+      v = a[m * W + k];
+      if (k > 0) v += ((which == 0) == !(k & 1) ? 1.0 : -1.0) * a[m * W - k];
+    } else {  // SC: row k, col l
+      const int k = row, l = col;
+      v = a[l * W + k];
+      if (l > 0) v += ((which == 2) == !(l & 1) ? 1.0 : -1.0) * a[-l * W + k];
+    }
+  }
+  out[gid] = v;
+}
+
+__device__ __forceinline__ void dmma(double2& d, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d.x), "+d"(d.y)
+               : "d"(a), "d"(b));
+}
+
+constexpr int ROT_WARPS = 4;
+constexpr int FRAG_KS_MAX = (P_MAX + 4) / 4;  // k-steps of the largest degree
+static_assert((P_MAX + 8) / 8 <= 3, "row tiles per degree");
+
+struct Frag {
+  double r[3][FRAG_KS_MAX], i[3][FRAG_KS_MAX];
+};
+
+// per offset: e^{-ik phi} (k <= P) and z_N = N! / |D|^(N+1) (N <= 2P)
+__global__ void k_rot_aux(const double* __restrict__ geo, int n_off, int P, double* __restrict__ aux) {
+  const int stride = aux_stride(P);
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)n_off * stride) return;
+  const int u = (int)(gid / stride), i = (int)(gid % stride);
+  const double r = geo[3 * u], phi = geo[3 * u + 2];
+  double v = 0.0;
+  if (i < 2 * (P + 1)) {
+    double sn, cs;
+    sincos(-(double)(i >> 1) * phi, &sn, &cs);
+    v = (i & 1) ? sn : cs;
+  } else if (i - 2 * (P + 1) <= 2 * P) {
+    const int N = i - 2 * (P + 1);
+    double f = 1.0, rp = 1.0 / r;
+    for (int t = 1; t <= N; ++t) {
+      f *= t;
+      rp /= r;
+    }
+    v = f * rp;
+  }
+  aux[gid] = v;
+}
+
+// warp unit = (item, octet of vectors); vector v of an item = (pair v / C, channel v % C).
+// Everything is unrolled for the compile-time order P; the next degree's operator
+// fragments are loaded while the current degree multiplies.
+template <int P>
+__global__ void __launch_bounds__(ROT_WARPS * 32)
+k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ gpair,
+          const int* __restrict__ pair_src, const double* __restrict__ frag, int ttot,
+          const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
           double2* __restrict__ pout) {
-  extern __shared__ double2 sh2[];
-  const int H = hcount(p), S = (p + 1) * (p + 1), RS = rot_size(p);
-  double2* sPh = sh2;                       // [2p+1] e^{-ik phi}, k = -p..p
-  double2* sMf = sPh + (2 * p + 1);         // [V][S] e^{-ik phi} M_n^k
-  double2* sMp = sMf + ROT_V * S;           // [V][H] M'
-  double2* sLp = sMp + ROT_V * H;           // [V][H] L'
-  double* sZ = reinterpret_cast<double*>(sLp + ROT_V * H);  // [2p+1] N! / r^(N+1)
-  double* sA = sZ + (2 * p + 2);                            // rotation matrices, 8-byte aligned
-  const int4 it = items[blockIdx.x];
+  constexpr int H = hcount(P);
+  constexpr int WS = 16 * H + 4 * P + 4;
+  extern __shared__ double sh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * ROT_WARPS + warp;
+  const int item = unit / C, oct = unit % C;
+  if (item >= n_items) return;
+  const int4 it = items[item];
+  const int nvec = (it.z - it.y) * C, v0 = oct * 8;
+  if (v0 >= nvec) return;
+  double* bre = sh + (size_t)warp * WS;                    // [H][8] real parts
+  double* bim = bre + 8 * H;                               // [H][8] imaginary parts
+  double2* ph = reinterpret_cast<double2*>(bim + 8 * H);   // [P+1] e^{-ik phi}
+  double* zz = reinterpret_cast<double*>(ph + P + 1);      // [2P+1] N! / r^(N+1)
   const int u = it.x;
   {
-    const double* A = rot + (size_t)u * rot_stride;
-    for (int i = threadIdx.x; i < RS; i += blockDim.x) cp_async8(sA + i, A + i);
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
-  const double r = geo[3 * u], ph = geo[3 * u + 2];
-  for (int k = threadIdx.x; k < 2 * p + 1; k += blockDim.x) {
-    double sn, cs;
-    sincos(-(double)(k - p) * ph, &sn, &cs);
-    sPh[k] = make_double2(cs, sn);
-  }
-  if (threadIdx.x == 0) {
-    double f = 1.0, rp = 1.0 / r;  // N! / r^(N+1)
-    for (int N = 0; N <= 2 * p; ++N) {
-      if (N > 0) {
-        f *= N;
-        rp /= r;
-      }
-      sZ[N] = f * rp;
-    }
-  }
-  const int vpp = C;                        // vectors per pair (channels)
-  const int ppass = ROT_V / vpp > 0 ? ROT_V / vpp : 1;
-  for (int e0 = it.y; e0 < it.z; e0 += ppass) {
-    const int np = min(ppass, it.z - e0);
-    const int nv = np * vpp;
-    __syncthreads();
-    for (int f = threadIdx.x; f < nv * S; f += blockDim.x) {
-      const int v = f / S, g = f - v * S;
-      const int e = gpair[e0 + v / vpp], c = v % vpp;
-      const int n = (int)__fsqrt_rz((float)g), k = g - n * n - n;
-      const double2 mv = hget(M + ((size_t)pair_src[e] * Ctot + c) * H, n, k);
-      sMf[v * S + g] = cmul(sPh[k + p], mv);
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
-    // stage A: M'_n^m = sum_k a^n_{mk} (e^{-ik phi} M_n^k), m >= 0, 4 vectors per item
-    const int ngrp = (nv + 3) / 4;
-    for (int w = threadIdx.x; w < H * ngrp; w += blockDim.x) {
-      const int idx = w % H, vg = w / H;
-      const int n = (int)((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
-      const int m = idx - n * (n + 1) / 2;
-      const double* arow = sA + rot_base(n) + (m + n) * (2 * n + 1) + n;  // a[k] at arow[k]
-      double2 acc[4] = {};
-      for (int k = -n; k <= n; ++k) {
-        const double aa = arow[k];
+    const double* A = aux + (size_t)u * aux_stride(aux_p);
+    double* sp = reinterpret_cast<double*>(ph);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2 mv = sMf[(vg * 4 + q) * S + n * n + n + k];
-          acc[q].x = fma(aa, mv.x, acc[q].x);
-          acc[q].y = fma(aa, mv.y, acc[q].y);
+    for (int i = lane; i < 2 * (P + 1); i += 32) sp[i] = A[i];
+#pragma unroll
+    for (int i = lane; i <= 2 * P; i += 32) zz[i] = A[2 * (aux_p + 1) + i];
+  }
+  const int fr = lane >> 2, fc = lane & 3;  // fragment row / column-in-k
+  const double* T = frag + (size_t)u * 4 * ttot * 32 + lane;
+  auto load = [&](Frag& f, int tab, int n) {
+    const int mt = frag_mt(n), ks = frag_ks(n);
+    const double* tr = T + (size_t)(tab * ttot + frag_base(n)) * 32;
+    const double* ti = tr + (size_t)ttot * 32;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int t = 0; t < FRAG_KS_MAX; ++t)
+        if (q < mt && t < ks) {
+          f.r[q][t] = __ldg(tr + (q * ks + t) * 32);
+          f.i[q][t] = __ldg(ti + (q * ks + t) * 32);
         }
-      }
+  };
+  Frag cur;
+  load(cur, 0, 0);
+  __syncwarp();
+  {  // stage in: Mf_n^k = e^{-ik phi} M_n^k, k >= 0, planar [h][v]
+    const int v = lane & 7, vg = v0 + v;
+    const double2* src = nullptr;
+    if (vg < nvec) src = M + ((size_t)pair_src[gpair[it.y + vg / C]] * C + vg % C) * H;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (vg * 4 + q < nv) sMp[(vg * 4 + q) * H + idx] = acc[q];
-    }
-    __syncthreads();
-    // stage B: L'_j^k = (-1)^j sum_{n>=k} M'_n^{-k} z_{n+j},  M'_n^{-k} = (-1)^k conj(M'_n^k)
-    for (int w = threadIdx.x; w < H * ngrp; w += blockDim.x) {
-      const int idx = w % H, vg = w / H;
-      const int j = (int)((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
-      const int k = idx - j * (j + 1) / 2;
-      double2 acc[4] = {};
-      for (int n = k; n <= p; ++n) {
-        const double zz = sZ[n + j];
-        const int hi = n * (n + 1) / 2 + k;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2 mv = sMp[(vg * 4 + q) * H + hi];
-          acc[q].x = fma(zz, mv.x, acc[q].x);
-          acc[q].y = fma(-zz, mv.y, acc[q].y);  // conj
+    for (int h0 = 0; h0 < H; h0 += 4) {
+      const int h = h0 + (lane >> 3);
+      if (h < H) {
+        double2 x = make_double2(0.0, 0.0);
+        if (src) {
+          const int n = (int)((sqrtf(8.0f * h + 1.0f) - 1.0f) * 0.5f);
+          x = cmul(ph[h - n * (n + 1) / 2], src[h]);
         }
-      }
-      const double sg = ((j + k) & 1) ? -1.0 : 1.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (vg * 4 + q < nv) sLp[(vg * 4 + q) * H + idx] = cscale(acc[q], sg);
-    }
-    __syncthreads();
-    // stage C: L_j^k = e^{-ik phi} sum_l a^j_{lk} L'_j^l (l < 0 via real symmetry)
-    for (int w = threadIdx.x; w < H * ngrp; w += blockDim.x) {
-      const int idx = w % H, vg = w / H;
-      const int j = (int)((sqrtf(8.0f * idx + 1.0f) - 1.0f) * 0.5f);
-      const int k = idx - j * (j + 1) / 2;
-      const double* acol = sA + rot_base(j) + (k + j);  // a[l][k] at acol[(l + j) * (2j + 1)]
-      const int stride = 2 * j + 1;
-      double2 acc[4] = {};
-      for (int l = -j; l <= j; ++l) {
-        const double aa = acol[(l + j) * stride];
-        const int al = l < 0 ? -l : l;
-        const int hi = j * (j + 1) / 2 + al;
-        const bool neg = l < 0, odd = (al & 1) != 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          double2 lv = sLp[(vg * 4 + q) * H + hi];
-          if (neg) lv = odd ? make_double2(-lv.x, lv.y) : make_double2(lv.x, -lv.y);
-          acc[q].x = fma(aa, lv.x, acc[q].x);
-          acc[q].y = fma(aa, lv.y, acc[q].y);
-        }
-      }
-      const double2 phs = sPh[k + p];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int v = vg * 4 + q;
-        if (v >= nv) continue;
-        const int e = gpair[e0 + v / vpp], c = v % vpp;
-        pout[((size_t)e * Ctot + c) * H + idx] = cmul(phs, acc[q]);
+        bre[h * 8 + v] = x.x;
+        bim[h * 8 + v] = x.y;
       }
     }
   }
+  __syncwarp();
+  double2 ar[3], ai[3];
+  // stage A (tables 0, 1) and stage C (tables 2, 3): out[row] = sum_col S[row][col] in[col]
+  auto mult = [&](const Frag& f, int n) {
+    const int mt = frag_mt(n), ks = frag_ks(n), hb = n * (n + 1) / 2;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) ar[q] = ai[q] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < FRAG_KS_MAX; ++t)
+      if (t < ks) {
+        const int col = t * 4 + fc;
+        const double br = col <= n ? bre[(hb + col) * 8 + fr] : 0.0;
+        const double bi = col <= n ? bim[(hb + col) * 8 + fr] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (q < mt) {
+            dmma(ar[q], f.r[q][t], br);
+            dmma(ai[q], f.i[q][t], bi);
+          }
+      }
+  };
+#pragma unroll
+  for (int n = 0; n <= P; ++n) {
+    Frag nxt;
+    if (n < P) load(nxt, 0, n + 1);
+    else load(nxt, 2, 0);  // stage C's first degree lands during stage B
+    mult(cur, n);
+    const int hb = n * (n + 1) / 2;
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int m = q * 8 + fr;
+      if (q < frag_mt(n) && m <= n) {
+        *reinterpret_cast<double2*>(bre + (hb + m) * 8 + 2 * fc) = ar[q];
+        *reinterpret_cast<double2*>(bim + (hb + m) * 8 + 2 * fc) = ai[q];
+      }
+    }
+    __syncwarp();
+    cur = nxt;
+  }
+  // stage B, per order k: rows j = k..P, reduction over n = k..P (Hankel operand z_{n+j})
+#pragma unroll
+  for (int k = 0; k <= P; ++k) {
+    const int L = P + 1 - k, jt = (L + 7) >> 3, ks = (L + 3) >> 2;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) ar[q] = ai[q] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < FRAG_KS_MAX; ++t)
+      if (t < ks) {
+        const int n = k + t * 4 + fc;
+        const bool ok = n <= P;
+        const int hn = n * (n + 1) / 2 + k;
+        const double br = ok ? bre[hn * 8 + fr] : 0.0;
+        const double bi = ok ? bim[hn * 8 + fr] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (q < jt) {
+            const int j = k + q * 8 + fr;
+            const double a = (ok && j <= P) ? zz[j + n] : 0.0;
+            dmma(ar[q], a, br);
+            dmma(ai[q], a, bi);
+          }
+      }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int j = k + q * 8 + fr;
+      if (q < jt && j <= P) {
+        const double sg = ((j + k) & 1) ? -1.0 : 1.0;
+        const int hj = j * (j + 1) / 2 + k;
+        *reinterpret_cast<double2*>(bre + hj * 8 + 2 * fc) = make_double2(sg * ar[q].x, sg * ar[q].y);
+        *reinterpret_cast<double2*>(bim + hj * 8 + 2 * fc) = make_double2(-sg * ai[q].x, -sg * ai[q].y);
+      }
+    }
+    __syncwarp();
+  }
+  // stage C and the output phase; lane owns vectors v0 + 2 fc and v0 + 2 fc + 1
+  double2* dst[2];
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const int vg = v0 + 2 * fc + w;
+    dst[w] = vg < nvec ? pout + ((size_t)gpair[it.y + vg / C] * C + vg % C) * H : nullptr;
+  }
+#pragma unroll
+  for (int j = 0; j <= P; ++j) {
+    Frag nxt;
+    if (j < P) load(nxt, 2, j + 1);
+    mult(cur, j);
+    const int hb = j * (j + 1) / 2;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int k = q * 8 + fr;
+      if (q < frag_mt(j) && k <= j) {
+        const double2 e = ph[k];
+        if (dst[0]) dst[0][hb + k] = cmul(e, make_double2(ar[q].x, ai[q].x));
+        if (dst[1]) dst[1][hb + k] = cmul(e, make_double2(ar[q].y, ai[q].y));
+      }
+    }
+    if (j < P) cur = nxt;
+  }
+}
+
+template <int P>
+void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int C,
+                  const double2* M, double2* pout, cudaStream_t st) {
+  constexpr int H = hcount(P);
+  const size_t smem = (size_t)ROT_WARPS * (16 * H + 4 * P + 4) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  const int64_t units = (int64_t)n_items * C;
+  k_m2l_rot<P><<<(unsigned)((units + ROT_WARPS - 1) / ROT_WARPS), ROT_WARPS * 32, smem, st>>>(
+      gitems, n_items, gpair, plan.m2l_src.get(), plan.rotf.get(), frag_base(plan.rot_p + 1),
+      plan.rot_aux.get(), plan.rot_p, M, C, pout);
+  FMM_LAUNCH_CHECK();
+}
+
+template <int... Ps>
+void launch_rot_dispatch(std::integer_sequence<int, Ps...>, int p, const Plan& plan,
+                         const int4* gitems, const int* gpair, int n_items, int C,
+                         const double2* M, double2* pout, cudaStream_t st) {
+  bool done = false;
+  ((p == Ps + M2L_ROT_MIN_P && !done
+        ? (launch_rot_p<Ps + M2L_ROT_MIN_P>(plan, gitems, gpair, n_items, C, M, pout, st), done = true)
+        : false),
+   ...);
+  FMM_REQUIRE(done, "rotation M2L order out of range");
 }
 
 }  // namespace
@@ -238,22 +397,27 @@ void compute_rot_tables(const double* d_off, int n_off, int P, double* out, doub
 
 size_t rot_table_size(int P) { return (size_t)rot_size(P); }
 
+size_t rot_frag_size(int P) { return (size_t)4 * frag_base(P + 1) * 32; }
+
+void build_rot_frag(const double* rot, int n_off, int P, double* out, cudaStream_t s) {
+  const int ttot = frag_base(P + 1);
+  const int64_t n = (int64_t)n_off * 4 * ttot * 32;
+  if (n) k_rot_frag<<<grid_for(n, 256), 256, 0, s>>>(rot, n_off, P, ttot, out);
+  FMM_LAUNCH_CHECK();
+}
+
+void build_rot_aux(const double* geo, int n_off, int P, double* aux, cudaStream_t s) {
+  const int64_t n = (int64_t)n_off * aux_stride(P);
+  if (n) k_rot_aux<<<grid_for(n, 128), 128, 0, s>>>(geo, n_off, P, aux);
+  FMM_LAUNCH_CHECK();
+}
+
 void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
                     int C, const double2* M, double2* pout, cudaStream_t st) {
   if (n_items <= 0) return;
-  const int H = hcount(p), S = (p + 1) * (p + 1);
-  const size_t smem = (size_t)(2 * p + 1 + ROT_V * S + 2 * ROT_V * H) * sizeof(double2) +
-                      (size_t)(2 * p + 2 + rot_size(p)) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
-  FMM_REQUIRE(smem <= 227 * 1024, "rotation M2L tiles exceed shared memory");
-  k_m2l_rot<<<n_items, ROT_THREADS, smem, st>>>(gitems, gpair, plan.m2l_src.get(), plan.rot.get(),
-                                               rot_size(plan.rot_p), plan.rot_geo.get(), p, M, C, C,
-                                               pout);
-  FMM_LAUNCH_CHECK();
+  FMM_REQUIRE(p <= plan.rot_p, "rotation tables not prepared for this order");
+  launch_rot_dispatch(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, plan, gitems,
+                      gpair, n_items, C, M, pout, st);
 }
 
 }  // namespace fmmbem

@@ -462,7 +462,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
                                           op.x_in.get(), op.y_out.get(), op.m2l_part.get(),
-                                          op.p2m_basis.get(), op.m2m_cout.get(), op.plan.rot.get()};
+                                          op.p2m_basis.get(), op.m2m_cout.get(), op.plan.rotf.get()};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;

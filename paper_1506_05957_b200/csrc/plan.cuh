@@ -69,6 +69,8 @@ struct Plan {
   // rotation-based M2L (m2l_rot.cu): per offset the scaled Wigner matrices a^n, n <= rot_p,
   // and (|D|, theta, phi)
   DevBuf<double> rot, rot_geo;
+  DevBuf<double> rot_aux;  // per offset e^{-ik phi} and N!/|D|^(N+1)
+  DevBuf<double> rotf;  // the same operators as DMMA 8x4 row fragments (m2l_rot.cu)
   int rot_p = -1;
   bool use_rot = true;  // FMMBEM_DENSE_M2L=1 selects the dense contraction instead
   // M2L work items: (target cell, pair begin, pair end, item id), <= 16 pairs each

@@ -203,6 +203,10 @@ void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
   plan.rot.resize((size_t)std::max(plan.n_offsets, 1) * rot_table_size(p));
   plan.rot_geo.resize((size_t)std::max(plan.n_offsets, 1) * 3);
   compute_rot_tables(plan.off_d.get(), plan.n_offsets, p, plan.rot.get(), plan.rot_geo.get(), s);
+  plan.rotf.resize((size_t)std::max(plan.n_offsets, 1) * rot_frag_size(p));
+  build_rot_frag(plan.rot.get(), plan.n_offsets, p, plan.rotf.get(), s);
+  plan.rot_aux.resize((size_t)std::max(plan.n_offsets, 1) * rot_aux_size(p));
+  build_rot_aux(plan.rot_geo.get(), plan.n_offsets, p, plan.rot_aux.get(), s);
   FMM_CUDA(cudaStreamSynchronize(s));
   plan.rot_p = p;
 }
