@@ -233,30 +233,127 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
           f.i[q][t] = __ldg(ti + (q * ks + t) * 32);
         }
   };
-  Frag cur;
-  load(cur, 0, 0);
-  __syncwarp();
-  {  // stage in: Mf_n^k = e^{-ik phi} M_n^k, k >= 0, planar [h][v]
-    const int v = lane & 7, vg = v0 + v;
-    const double2* src = nullptr;
-    if (vg < nvec) src = M + ((size_t)pair_src[gpair[it.y + vg / C]] * C + vg % C) * H;
+  // stage A: Re/Im M'_n^m = SA_re/im[m][k] Re/Im (e^{-ik phi} M_n^k); the B operand
+  // (k = 4t + fc, vector fr) comes straight from global memory, so the degrees are
+  // independent and need no synchronisation; next degree's operands are in flight
+  const double2* msrc = nullptr;
+  {
+    const int vg = v0 + fr;
+    if (vg < nvec) msrc = M + ((size_t)pair_src[gpair[it.y + vg / C]] * C + vg % C) * H;
+  }
+  __syncwarp();  // ph, zz
+  struct BIn {
+    double2 m[FRAG_KS_MAX];
+  };
+  auto load_b = [&](BIn& b, int n) {
+    const int ks = frag_ks(n), hb = n * (n + 1) / 2;
 #pragma unroll
-    for (int h0 = 0; h0 < H; h0 += 4) {
-      const int h = h0 + (lane >> 3);
-      if (h < H) {
-        double2 x = make_double2(0.0, 0.0);
-        if (src) {
-          const int n = (int)((sqrtf(8.0f * h + 1.0f) - 1.0f) * 0.5f);
-          x = cmul(ph[h - n * (n + 1) / 2], src[h]);
+    for (int t = 0; t < FRAG_KS_MAX; ++t)
+      if (t < ks) {
+        const int col = t * 4 + fc;
+        b.m[t] = (msrc && col <= n) ? __ldg(msrc + hb + col) : make_double2(0.0, 0.0);
+      }
+  };
+  double2 ar[3], ai[3];
+  auto mult_a = [&](const Frag& f, const BIn& b, int n) {
+    const int mt = frag_mt(n), ks = frag_ks(n);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) ar[q] = ai[q] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < FRAG_KS_MAX; ++t)
+      if (t < ks) {
+        const int col = t * 4 + fc;
+        const double2 x = col <= n ? cmul(ph[col], b.m[t]) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (q < mt) {
+            dmma(ar[q], f.r[q][t], x.x);
+            dmma(ai[q], f.i[q][t], x.y);
+          }
+      }
+  };
+  {
+    Frag cur;
+    BIn bc;
+    load(cur, 0, 0);
+    load_b(bc, 0);
+#pragma unroll
+    for (int n = 0; n <= P; ++n) {
+      Frag nxt;
+      BIn bn;
+      if (n < P) {
+        load(nxt, 0, n + 1);
+        load_b(bn, n + 1);
+      }
+      mult_a(cur, bc, n);
+      const int hb = n * (n + 1) / 2;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int m = q * 8 + fr;
+        if (q < frag_mt(n) && m <= n) {
+          *reinterpret_cast<double2*>(bre + (hb + m) * 8 + 2 * fc) = ar[q];
+          *reinterpret_cast<double2*>(bim + (hb + m) * 8 + 2 * fc) = ai[q];
         }
-        bre[h * 8 + v] = x.x;
-        bim[h * 8 + v] = x.y;
+      }
+      if (n < P) {
+        cur = nxt;
+        bc = bn;
       }
     }
   }
+  Frag cur;
+  load(cur, 2, 0);  // stage C's first degree lands during stage B
   __syncwarp();
-  double2 ar[3], ai[3];
-  // stage A (tables 0, 1) and stage C (tables 2, 3): out[row] = sum_col S[row][col] in[col]
+  // stage B, two orders per pass: rows j = k..P, reduction over n = k..P, Hankel
+  // operand (-1)^(j+k) z_{n+j} (negated for the conjugated imaginary part)
+#pragma unroll
+  for (int k0 = 0; k0 <= P; k0 += 2) {
+    double2 br_[2][3], bi_[2][3];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int k = k0 + w;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) br_[w][q] = bi_[w][q] = make_double2(0.0, 0.0);
+      if (k > P) continue;
+      const int L = P + 1 - k, jt = (L + 7) >> 3, ks = (L + 3) >> 2;
+#pragma unroll
+      for (int t = 0; t < FRAG_KS_MAX; ++t)
+        if (t < ks) {
+          const int n = k + t * 4 + fc;
+          const bool ok = n <= P;
+          const int hn = n * (n + 1) / 2 + k;
+          const double vr = ok ? bre[hn * 8 + fr] : 0.0;
+          const double vi = ok ? bim[hn * 8 + fr] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (q < jt) {
+              const int j = k + q * 8 + fr;
+              double a = (ok && j <= P) ? zz[j + n] : 0.0;
+              if ((j + k) & 1) a = -a;
+              dmma(br_[w][q], a, vr);
+              dmma(bi_[w][q], -a, vi);
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int k = k0 + w;
+      if (k > P) continue;
+      const int jt = (P + 1 - k + 7) >> 3;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int j = k + q * 8 + fr;
+        if (q < jt && j <= P) {
+          const int hj = j * (j + 1) / 2 + k;
+          *reinterpret_cast<double2*>(bre + hj * 8 + 2 * fc) = br_[w][q];
+          *reinterpret_cast<double2*>(bim + hj * 8 + 2 * fc) = bi_[w][q];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // stage C (tables 2, 3): Re/Im L~_j^k = SC_re/im[k][l] Re/Im L'_j^l
   auto mult = [&](const Frag& f, int n) {
     const int mt = frag_mt(n), ks = frag_ks(n), hb = n * (n + 1) / 2;
 #pragma unroll
@@ -275,61 +372,6 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
           }
       }
   };
-#pragma unroll
-  for (int n = 0; n <= P; ++n) {
-    Frag nxt;
-    if (n < P) load(nxt, 0, n + 1);
-    else load(nxt, 2, 0);  // stage C's first degree lands during stage B
-    mult(cur, n);
-    const int hb = n * (n + 1) / 2;
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int m = q * 8 + fr;
-      if (q < frag_mt(n) && m <= n) {
-        *reinterpret_cast<double2*>(bre + (hb + m) * 8 + 2 * fc) = ar[q];
-        *reinterpret_cast<double2*>(bim + (hb + m) * 8 + 2 * fc) = ai[q];
-      }
-    }
-    __syncwarp();
-    cur = nxt;
-  }
-  // stage B, per order k: rows j = k..P, reduction over n = k..P (Hankel operand z_{n+j})
-#pragma unroll
-  for (int k = 0; k <= P; ++k) {
-    const int L = P + 1 - k, jt = (L + 7) >> 3, ks = (L + 3) >> 2;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) ar[q] = ai[q] = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int t = 0; t < FRAG_KS_MAX; ++t)
-      if (t < ks) {
-        const int n = k + t * 4 + fc;
-        const bool ok = n <= P;
-        const int hn = n * (n + 1) / 2 + k;
-        const double br = ok ? bre[hn * 8 + fr] : 0.0;
-        const double bi = ok ? bim[hn * 8 + fr] : 0.0;
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-          if (q < jt) {
-            const int j = k + q * 8 + fr;
-            const double a = (ok && j <= P) ? zz[j + n] : 0.0;
-            dmma(ar[q], a, br);
-            dmma(ai[q], a, bi);
-          }
-      }
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const int j = k + q * 8 + fr;
-      if (q < jt && j <= P) {
-        const double sg = ((j + k) & 1) ? -1.0 : 1.0;
-        const int hj = j * (j + 1) / 2 + k;
-        *reinterpret_cast<double2*>(bre + hj * 8 + 2 * fc) = make_double2(sg * ar[q].x, sg * ar[q].y);
-        *reinterpret_cast<double2*>(bim + hj * 8 + 2 * fc) = make_double2(-sg * ai[q].x, -sg * ai[q].y);
-      }
-    }
-    __syncwarp();
-  }
   // stage C and the output phase; lane owns vectors v0 + 2 fc and v0 + 2 fc + 1
   double2* dst[2];
 #pragma unroll

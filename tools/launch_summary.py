@@ -1,6 +1,6 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) per kernel.
 
-Usage: python tools/launch_summary.py gpurun_out/launches.csv [--skip-setup]
+Usage: python tools/launch_summary.py gpurun_out/launches.csv [--skip-setup] [--tail N]
 Prints kernel, launches, total/avg duration (us) and share of the listed time.
 ncu launch times are cold-cache and serialised: compare SHARES, not absolutes.
 """
@@ -16,7 +16,7 @@ SETUP = ("k_bbox", "k_path_keys", "k_classify", "k_heads", "k_emit", "k_child_co
          "k_sorted_sources", "cub::", "k_dfma_probe", "at::", "k_permute")
 
 
-def main(path, skip_setup=False):
+def main(path, skip_setup=False, tail=0):
     rows = list(csv.reader(open(path)))
     hdr, data = None, []
     for r in rows:
@@ -26,7 +26,8 @@ def main(path, skip_setup=False):
         if hdr and len(r) == len(hdr):
             data.append(dict(zip(hdr, r)))
     agg = collections.defaultdict(lambda: [0, 0.0])
-    for d in data:
+    data = [d for d in data if d["Metric Name"] == "gpu__time_duration.sum"]
+    for d in data[-tail:] if tail else data:
         if d["Metric Name"] != "gpu__time_duration.sum":
             continue
         name = d["Kernel Name"].split("(")[0].replace("fmmbem::", "").replace("<unnamed>::", "")
@@ -42,4 +43,5 @@ def main(path, skip_setup=False):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], "--skip-setup" in sys.argv)
+    a = sys.argv
+    main(a[1], "--skip-setup" in a, int(a[a.index("--tail") + 1]) if "--tail" in a else 0)
