@@ -95,6 +95,12 @@ struct BemOp {
   int basis_p = -1;
   bool use_basis = false;
   DevBuf<double2> p2m_basis;
+  // Laplace kinds: the Gauss points of one panel inside one leaf share x[panel],
+  // so their basis columns are pre-summed per (leaf, panel) cluster
+  bool basis_clustered = false;
+  int basis_cols = 0;            // columns of p2m_basis (clusters or sources)
+  DevBuf<int> cl_range;          // per source cell: first cluster, one past last (2 per cell)
+  DevBuf<int> cl_panel;          // per cluster: panel index
 
   // GMRES workspaces (Krylov basis, reductions), grow-only
   DevBuf<double> g_basis, g_partials, g_scal, g_y;

@@ -112,6 +112,38 @@ k_p2m_basis(const int* __restrict__ leaves, const int* __restrict__ body_start,
   }
 }
 
+// clustered columns (Laplace kinds, one channel), cluster-major Bc[c][h]:
+// M_leaf[h] = sum over the leaf's clusters of Bc[c][h] x[panel(c)], one thread per h
+__global__ void __launch_bounds__(128)
+k_p2m_basis_cl(const int* __restrict__ leaves, const int2* __restrict__ cl_range, int Hp, int H,
+               const double2* __restrict__ B, const int* __restrict__ cl_panel,
+               const double* __restrict__ x, double2* __restrict__ M) {
+  const int leaf = leaves[blockIdx.x];
+  const int2 cr = cl_range[leaf];
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int c = cr.x; c < cr.y; ++c) {
+      const double s = __ldg(x + __ldg(cl_panel + c));
+      const double2 v = __ldg(B + (size_t)c * Hp + h);
+      acc.x = fma(s, v.x, acc.x);
+      acc.y = fma(s, v.y, acc.y);
+    }
+    M[(size_t)leaf * H + h] = acc;
+  }
+}
+
+// Bc[c][h] = sum over the cluster's Gauss points (in sorted order) of B[h][i]
+__global__ void k_basis_cluster_sum(int64_t ns, int ncl, int H, const int* __restrict__ cl_src,
+                                    const double2* __restrict__ B, double2* __restrict__ Bc) {
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)ncl * H) return;
+  const int h = (int)(gid % H), c = (int)(gid / H);
+  double2 a = make_double2(0.0, 0.0);
+  for (int i = cl_src[c]; i < cl_src[c + 1]; ++i) a = cadd(a, B[(size_t)h * ns + i]);
+  Bc[(size_t)c * H + h] = a;
+}
+
 }  // namespace
 
 bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s) {
@@ -121,14 +153,44 @@ bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s) {
   const int ptab = std::max(p, std::min(P_MAX, std::max(op.basis_p, 12)));
   constexpr double BUDGET = 24e9;  // bytes of HBM this table may take
   if ((double)hcount(ptab) * ns * sizeof(double2) > BUDGET) return false;
-  op.p2m_basis.resize((size_t)hcount(ptab) * ns);
   const Tree& S = op.plan.src;
+  const bool cluster = op.basis_kind_for_sys == K_LAP_SINGLE || op.basis_kind_for_sys == K_LAP_DOUBLE;
+  DevBuf<double2> per_source;
+  DevBuf<double2>& B = cluster ? per_source : op.p2m_basis;
+  B.resize((size_t)hcount(ptab) * ns);
   k_basis_build<<<grid_for(ns, 128), 128, 0, s>>>(ns, ptab, op.basis_kind_for_sys, S.px.get(),
                                                   S.py.get(), S.pz.get(), S.leaf_of_body.get(),
                                                   S.cx.get(), S.cy.get(), S.cz.get(),
                                                   op.s_weight.get(), op.s_panel.get(),
-                                                  op.normal.get(), S.rec, op.p2m_basis.get());
+                                                  op.normal.get(), S.rec, B.get());
   FMM_LAUNCH_CHECK();
+  op.basis_clustered = cluster;
+  op.basis_cols = (int)ns;
+  if (cluster) {
+    // clusters: maximal runs of sorted Gauss points with the same (leaf, panel)
+    const std::vector<int> leaf = S.leaf_of_body.download(s), pan = op.s_panel.download(s);
+    std::vector<int> src_begin, cpanel, range(2 * (size_t)S.n_cells, 0);
+    for (int64_t i = 0; i < ns; ++i) {
+      if (i == 0 || leaf[i] != leaf[i - 1] || pan[i] != pan[i - 1]) {
+        if (i == 0 || leaf[i] != leaf[i - 1]) range[2 * (size_t)leaf[i]] = (int)src_begin.size();
+        src_begin.push_back((int)i);
+        cpanel.push_back(pan[i]);
+      }
+      range[2 * (size_t)leaf[i] + 1] = (int)src_begin.size();
+    }
+    const int ncl = (int)cpanel.size();
+    src_begin.push_back((int)ns);
+    DevBuf<int> d_src;
+    d_src.upload(src_begin, s);
+    op.cl_panel.upload(cpanel, s);
+    op.cl_range.upload(range, s);
+    op.p2m_basis.resize((size_t)hcount(ptab) * ncl);
+    const int64_t n = (int64_t)ncl * hcount(ptab);
+    k_basis_cluster_sum<<<grid_for(n, 256), 256, 0, s>>>(ns, ncl, hcount(ptab), d_src.get(),
+                                                          per_source.get(), op.p2m_basis.get());
+    FMM_LAUNCH_CHECK();
+    op.basis_cols = ncl;
+  }
   FMM_CUDA(cudaStreamSynchronize(s));
   op.basis_p = ptab;
   return true;
@@ -143,7 +205,12 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
     n_leaves = S.n_leaves;
   }
   if (n_leaves <= 0) return;
-  if (C == 1)
+  if (op.basis_clustered) {
+    FMM_REQUIRE(C == 1, "clustered P2M basis is single-channel");
+    k_p2m_basis_cl<<<n_leaves, 128, 0, s>>>(leaves, reinterpret_cast<const int2*>(op.cl_range.get()),
+                                             hcount(op.basis_p), H, op.p2m_basis.get(), op.cl_panel.get(),
+                                             x, M);
+  } else if (C == 1)
     k_p2m_basis<1><<<n_leaves, 256, 0, s>>>(leaves, S.body_start.get(), S.body_count.get(),
                                               S.n_points, H, op.basis_kind_for_sys,
                                               op.p2m_basis.get(), op.s_panel.get(), x, S.px.get(),
