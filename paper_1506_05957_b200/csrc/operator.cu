@@ -371,12 +371,18 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     const bool own_only = sharded && !sw.virtual_mode;  // P2M of own leaves, then all-gather
     const int* lv = own_only ? sw.p2m_leaves.get() : pl.src.leaves.get();
     const int nlv = own_only ? sw.n_p2m_leaves : pl.src.n_leaves;
-    if (c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p)
-      launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, lv, nlv);
-    else
-      launch_p2m(S, lv, nlv, c.p, C, q, d, op.M.get(), s);
-    if (own_only) shard_exchange_multipoles(op, C, c.p, s);
-    launch_m2m_grouped(pl, c.p, C, pl.rshift_src.get(), op.M.get(), op.m2m_cout.get(), s);
+    const bool basis = c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p;
+    if (basis && op.basis_clustered && !own_only) {
+      // every multipole straight from the sources (no M2M levels)
+      launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, nullptr, 0);
+    } else {
+      if (basis)
+        launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, lv, nlv);
+      else
+        launch_p2m(S, lv, nlv, c.p, C, q, d, op.M.get(), s);
+      if (own_only) shard_exchange_multipoles(op, C, c.p, s);
+      launch_m2m_grouped(pl, c.p, C, pl.rshift_src.get(), op.M.get(), op.m2m_cout.get(), s);
+    }
     record(op, ST_UP, true, s);
     record(op, ST_M2L, false, s);
     if (sharded)
@@ -462,7 +468,9 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
                                           op.x_in.get(), op.y_out.get(), op.m2l_part.get(),
-                                          op.p2m_basis.get(), op.m2m_cout.get(), op.plan.rotf.get()};
+                                          op.p2m_basis.get(), op.m2m_cout.get(), op.plan.rotf.get(),
+                                          op.plan.rot_aux.get(), op.cl_panel.get(),
+                                          op.p2m_items.d.get(), op.p2m_reduce.d.get(), op.p2m_part.get()};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;

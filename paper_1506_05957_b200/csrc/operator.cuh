@@ -52,6 +52,11 @@ struct ShardWork {
   void* comm = nullptr;
 };
 
+struct P2MItems {
+  DevBuf<int4> d;
+  int n = 0;
+};
+
 struct BemOp {
   int formulation = LAPLACE_SECOND;
   double mu = 1e-3;
@@ -99,8 +104,15 @@ struct BemOp {
   // so their basis columns are pre-summed per (leaf, panel) cluster
   bool basis_clustered = false;
   int basis_cols = 0;            // columns of p2m_basis (clusters or sources)
-  DevBuf<int> cl_range;          // per source cell: first cluster, one past last (2 per cell)
-  DevBuf<int> cl_panel;          // per cluster: panel index
+  // direct upward pass (clustered kinds): basis entries (cell, cluster of its subtree)
+  // for every M2L source cell and leaf, so the multipoles need no M2M
+  std::vector<int> h_cl_range;   // per source cell: first entry, one past last (2 per cell)
+  DevBuf<int> cl_panel;          // per entry: panel index
+  P2MItems p2m_items, p2m_reduce;            // all multipoles (unsharded)
+  P2MItems p2m_leaf_items, p2m_leaf_reduce;  // a shard's own leaves
+  const int* p2m_leaf_list = nullptr;
+  int n_p2m_slots = 0, n_p2m_leaf_slots = 0;
+  DevBuf<double2> p2m_part;
 
   // GMRES workspaces (Krylov basis, reductions), grow-only
   DevBuf<double> g_basis, g_partials, g_scal, g_y;

@@ -13,6 +13,8 @@
 // once per operator; every apply is a coalesced streaming reduction over it:
 // one warp per (leaf, coefficient), lanes over the leaf's Gauss points,
 // shuffle-tree reduction in a fixed order.
+#include <algorithm>
+
 #include "operator.cuh"
 
 namespace fmmbem {
@@ -112,39 +114,109 @@ k_p2m_basis(const int* __restrict__ leaves, const int* __restrict__ body_start,
   }
 }
 
-// clustered columns (Laplace kinds, one channel), cluster-major Bc[c][h]:
-// M_leaf[h] = sum over the leaf's clusters of Bc[c][h] x[panel(c)], one thread per h
+// clustered entries (Laplace kinds, one channel), entry-major Bd[e][h]: work item
+// (cell, entry range, slot): acc[h] = sum_e Bd[e][h] x[panel(e)], one thread per h;
+// slot < 0 writes the cell's multipole, else a partial that k_p2m_reduce adds in order
 __global__ void __launch_bounds__(128)
-k_p2m_basis_cl(const int* __restrict__ leaves, const int2* __restrict__ cl_range, int Hp, int H,
-               const double2* __restrict__ B, const int* __restrict__ cl_panel,
-               const double* __restrict__ x, double2* __restrict__ M) {
-  const int leaf = leaves[blockIdx.x];
-  const int2 cr = cl_range[leaf];
+k_p2m_basis_cl(const int4* __restrict__ items, int Hp, int H, const double2* __restrict__ B,
+               const int* __restrict__ e_panel, const double* __restrict__ x,
+               double2* __restrict__ M, double2* __restrict__ part) {
+  const int4 it = items[blockIdx.x];
+  double2* out = it.w < 0 ? M + (size_t)it.x * H : part + (size_t)it.w * H;
   for (int h = threadIdx.x; h < H; h += blockDim.x) {
     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll 4
-    for (int c = cr.x; c < cr.y; ++c) {
-      const double s = __ldg(x + __ldg(cl_panel + c));
-      const double2 v = __ldg(B + (size_t)c * Hp + h);
+    for (int e = it.y; e < it.z; ++e) {
+      const double s = __ldg(x + __ldg(e_panel + e));
+      const double2 v = __ldg(B + (size_t)e * Hp + h);
       acc.x = fma(s, v.x, acc.x);
       acc.y = fma(s, v.y, acc.y);
     }
-    M[(size_t)leaf * H + h] = acc;
+    out[h] = acc;
   }
 }
 
-// Bc[c][h] = sum over the cluster's Gauss points (in sorted order) of B[h][i]
-__global__ void k_basis_cluster_sum(int64_t ns, int ncl, int H, const int* __restrict__ cl_src,
-                                    const double2* __restrict__ B, double2* __restrict__ Bc) {
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)ncl * H) return;
-  const int h = (int)(gid % H), c = (int)(gid / H);
-  double2 a = make_double2(0.0, 0.0);
-  for (int i = cl_src[c]; i < cl_src[c + 1]; ++i) a = cadd(a, B[(size_t)h * ns + i]);
-  Bc[(size_t)c * H + h] = a;
+// cells split over several items: (cell, first slot, slot count)
+__global__ void k_p2m_reduce(const int4* __restrict__ cells, int H, const double2* __restrict__ part,
+                             double2* __restrict__ M) {
+  const int4 c = cells[blockIdx.x];
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    double2 acc = part[(size_t)c.y * H + h];
+    for (int k = 1; k < c.z; ++k) acc = cadd(acc, part[(size_t)(c.y + k) * H + h]);
+    M[(size_t)c.x * H + h] = acc;
+  }
+}
+
+// Direct upward basis: entry e = (cell, cluster in the cell's subtree),
+// Bd[e][h] = sum over the cluster's Gauss points (sorted order) of the kernel's
+// P2M basis about the CELL's centre.  M2M of a regular-harmonic expansion is
+// exact (degree j of the parent only needs degrees <= j of the child), so this
+// is the multipole the M2M chain would produce, with no level dependencies.
+__global__ void k_basis_build_entries(int ne, int ptab, int kind, const int* __restrict__ e_cell,
+                                      const int* __restrict__ e_cluster, const int* __restrict__ cl_src,
+                                      const double* __restrict__ px, const double* __restrict__ py,
+                                      const double* __restrict__ pz, const double* __restrict__ cx,
+                                      const double* __restrict__ cy, const double* __restrict__ cz,
+                                      const double* __restrict__ s_w, const int* __restrict__ s_panel,
+                                      const double* __restrict__ nrm, const double* __restrict__ rec,
+                                      double2* __restrict__ B) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const int cell = e_cell[e], cl = e_cluster[e];
+  const int H = hcount(ptab);
+  double2 R[hcount(P_MAX)], acc[hcount(P_MAX)];
+  for (int h = 0; h < H; ++h) acc[h] = make_double2(0.0, 0.0);
+  for (int i = cl_src[cl]; i < cl_src[cl + 1]; ++i) {
+    regular_half(px[i] - cx[cell], py[i] - cy[cell], pz[i] - cz[cell], ptab, R, rec);
+    const double w = s_w[i];
+    if (kind != K_LAP_DOUBLE) {
+      for (int h = 0; h < H; ++h) acc[h] = cadd(acc[h], cscale(R[h], w));
+      continue;
+    }
+    const int pn = s_panel[i];
+    const double dx = 0.5 * w * nrm[3 * pn], dy = 0.5 * w * nrm[3 * pn + 1], dz = w * nrm[3 * pn + 2];
+    for (int n = 1; n <= ptab; ++n)
+      for (int m = 0; m <= n; ++m) {
+        double2 a = make_double2(0.0, 0.0);
+        if (m + 1 <= n - 1) a = cfma(make_double2(dx, -dy), R[hidx(n - 1, m + 1)], a);
+        if (m - 1 >= -(n - 1)) a = cfma(make_double2(-dx, -dy), hget(R, n - 1, m - 1), a);
+        if (m <= n - 1) {
+          const double2 r = R[hidx(n - 1, m)];
+          a.x = fma(dz, r.x, a.x);
+          a.y = fma(dz, r.y, a.y);
+        }
+        acc[hidx(n, m)] = cadd(acc[hidx(n, m)], a);
+      }
+  }
+  for (int h = 0; h < H; ++h) B[(size_t)e * H + h] = acc[h];
 }
 
 }  // namespace
+
+// work items over the entries of the given cells, <= P2M_CHUNK entries each
+void set_p2m_items(BemOp& op, const std::vector<int>& cells, const std::vector<int>& range,
+                   P2MItems& items, P2MItems& reduce, int& n_slots) {
+  constexpr int P2M_CHUNK = 32;
+  std::vector<int4> it, red;
+  int slot = 0;
+  for (int c : cells) {
+    const int e0 = range[2 * (size_t)c], e1 = range[2 * (size_t)c + 1], len = e1 - e0;
+    const int nch = std::max(1, (len + P2M_CHUNK - 1) / P2M_CHUNK);
+    if (nch == 1) {
+      it.push_back(make_int4(c, e0, e1, -1));
+      continue;
+    }
+    red.push_back(make_int4(c, slot, nch, 0));
+    for (int q = 0; q < nch; ++q)
+      it.push_back(make_int4(c, e0 + (int)((int64_t)len * q / nch), e0 + (int)((int64_t)len * (q + 1) / nch),
+                             slot++));
+  }
+  items.n = (int)it.size();
+  items.d.upload(it.empty() ? std::vector<int4>(1) : it);
+  reduce.n = (int)red.size();
+  reduce.d.upload(red.empty() ? std::vector<int4>(1) : red);
+  n_slots = slot;
+}
 
 bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s) {
   if (op.basis_p >= p) return true;
@@ -155,41 +227,66 @@ bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s) {
   if ((double)hcount(ptab) * ns * sizeof(double2) > BUDGET) return false;
   const Tree& S = op.plan.src;
   const bool cluster = op.basis_kind_for_sys == K_LAP_SINGLE || op.basis_kind_for_sys == K_LAP_DOUBLE;
-  DevBuf<double2> per_source;
-  DevBuf<double2>& B = cluster ? per_source : op.p2m_basis;
-  B.resize((size_t)hcount(ptab) * ns);
-  k_basis_build<<<grid_for(ns, 128), 128, 0, s>>>(ns, ptab, op.basis_kind_for_sys, S.px.get(),
-                                                  S.py.get(), S.pz.get(), S.leaf_of_body.get(),
-                                                  S.cx.get(), S.cy.get(), S.cz.get(),
-                                                  op.s_weight.get(), op.s_panel.get(),
-                                                  op.normal.get(), S.rec, B.get());
-  FMM_LAUNCH_CHECK();
   op.basis_clustered = cluster;
-  op.basis_cols = (int)ns;
-  if (cluster) {
+  if (!cluster) {
+    op.p2m_basis.resize((size_t)hcount(ptab) * ns);
+    k_basis_build<<<grid_for(ns, 128), 128, 0, s>>>(ns, ptab, op.basis_kind_for_sys, S.px.get(),
+                                                    S.py.get(), S.pz.get(), S.leaf_of_body.get(),
+                                                    S.cx.get(), S.cy.get(), S.cz.get(),
+                                                    op.s_weight.get(), op.s_panel.get(),
+                                                    op.normal.get(), S.rec, op.p2m_basis.get());
+    FMM_LAUNCH_CHECK();
+    op.basis_cols = (int)ns;
+  } else {
     // clusters: maximal runs of sorted Gauss points with the same (leaf, panel)
     const std::vector<int> leaf = S.leaf_of_body.download(s), pan = op.s_panel.download(s);
-    std::vector<int> src_begin, cpanel, range(2 * (size_t)S.n_cells, 0);
-    for (int64_t i = 0; i < ns; ++i) {
+    std::vector<int> src_begin, cpanel;
+    for (int64_t i = 0; i < ns; ++i)
       if (i == 0 || leaf[i] != leaf[i - 1] || pan[i] != pan[i - 1]) {
-        if (i == 0 || leaf[i] != leaf[i - 1]) range[2 * (size_t)leaf[i]] = (int)src_begin.size();
         src_begin.push_back((int)i);
         cpanel.push_back(pan[i]);
       }
-      range[2 * (size_t)leaf[i] + 1] = (int)src_begin.size();
-    }
-    const int ncl = (int)cpanel.size();
     src_begin.push_back((int)ns);
-    DevBuf<int> d_src;
+    // cells with a multipole: every M2L source and every leaf (the sharded path's P2M)
+    const Plan& pl = op.plan;
+    std::vector<char> need(S.n_cells, 0);
+    for (int c : pl.h_m2l_src) need[c] = 1;
+    for (int c = 0; c < S.n_cells; ++c)
+      if (S.h_n_child[c] == 0) need[c] = 1;
+    std::vector<int> cells, e_cell, e_cl, e_panel, range(2 * (size_t)S.n_cells, 0);
+    for (int c = 0; c < S.n_cells; ++c) {
+      if (!need[c]) continue;
+      cells.push_back(c);
+      const int b0 = S.h_body_start[c], b1 = b0 + S.h_body_count[c];
+      const int k0 = (int)(std::lower_bound(src_begin.begin(), src_begin.end(), b0) - src_begin.begin());
+      const int k1 = (int)(std::lower_bound(src_begin.begin(), src_begin.end(), b1) - src_begin.begin());
+      range[2 * (size_t)c] = (int)e_cell.size();
+      for (int k = k0; k < k1; ++k) {
+        e_cell.push_back(c);
+        e_cl.push_back(k);
+        e_panel.push_back(cpanel[k]);
+      }
+      range[2 * (size_t)c + 1] = (int)e_cell.size();
+    }
+    const int ne = (int)e_cell.size();
+    if ((double)hcount(ptab) * ne * sizeof(double2) > BUDGET) return false;
+    DevBuf<int> d_src, d_cell, d_cl;
     d_src.upload(src_begin, s);
-    op.cl_panel.upload(cpanel, s);
-    op.cl_range.upload(range, s);
-    op.p2m_basis.resize((size_t)hcount(ptab) * ncl);
-    const int64_t n = (int64_t)ncl * hcount(ptab);
-    k_basis_cluster_sum<<<grid_for(n, 256), 256, 0, s>>>(ns, ncl, hcount(ptab), d_src.get(),
-                                                          per_source.get(), op.p2m_basis.get());
+    d_cell.upload(e_cell, s);
+    d_cl.upload(e_cl, s);
+    op.cl_panel.upload(e_panel, s);
+    op.h_cl_range = range;
+    set_p2m_items(op, cells, range, op.p2m_items, op.p2m_reduce, op.n_p2m_slots);
+    op.p2m_part.ensure((size_t)std::max(op.n_p2m_slots, 1) * hcount(P_MAX));
+    op.p2m_leaf_list = nullptr;
+    op.p2m_basis.resize((size_t)hcount(ptab) * ne);
+    k_basis_build_entries<<<grid_for(ne, 64), 64, 0, s>>>(
+        ne, ptab, op.basis_kind_for_sys, d_cell.get(), d_cl.get(), d_src.get(), S.px.get(),
+        S.py.get(), S.pz.get(), S.cx.get(), S.cy.get(), S.cz.get(), op.s_weight.get(),
+        op.s_panel.get(), op.normal.get(), S.rec, op.p2m_basis.get());
     FMM_LAUNCH_CHECK();
-    op.basis_cols = ncl;
+    op.basis_cols = ne;
+    FMM_CUDA(cudaStreamSynchronize(s));
   }
   FMM_CUDA(cudaStreamSynchronize(s));
   op.basis_p = ptab;
@@ -200,17 +297,32 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
                       const int* leaves, int n_leaves) {
   const Tree& S = op.plan.src;
   const int H = hcount(p);
-  if (!leaves) {
-    leaves = S.leaves.get();
-    n_leaves = S.n_leaves;
-  }
-  if (n_leaves <= 0) return;
   if (op.basis_clustered) {
     FMM_REQUIRE(C == 1, "clustered P2M basis is single-channel");
-    k_p2m_basis_cl<<<n_leaves, 128, 0, s>>>(leaves, reinterpret_cast<const int2*>(op.cl_range.get()),
-                                             hcount(op.basis_p), H, op.p2m_basis.get(), op.cl_panel.get(),
-                                             x, M);
-  } else if (C == 1)
+    const bool direct = leaves == nullptr;  // all multipoles, else the given leaves
+    if (!direct && leaves != op.p2m_leaf_list) {  // a shard's leaf list (not under capture)
+      std::vector<int> lv(n_leaves);
+      if (n_leaves)
+        FMM_CUDA(cudaMemcpy(lv.data(), leaves, n_leaves * sizeof(int), cudaMemcpyDeviceToHost));
+      set_p2m_items(op, lv, op.h_cl_range, op.p2m_leaf_items, op.p2m_leaf_reduce, op.n_p2m_leaf_slots);
+      op.p2m_part.ensure((size_t)std::max(op.n_p2m_leaf_slots, 1) * hcount(P_MAX));
+      op.p2m_leaf_list = leaves;
+    }
+    const P2MItems& it = direct ? op.p2m_items : op.p2m_leaf_items;
+    const P2MItems& red = direct ? op.p2m_reduce : op.p2m_leaf_reduce;
+    FMM_REQUIRE(op.p2m_part.size() >= (size_t)std::max(op.n_p2m_slots, op.n_p2m_leaf_slots) * H,
+                "P2M partial buffer not sized");
+    if (it.n)
+      k_p2m_basis_cl<<<it.n, 128, 0, s>>>(it.d.get(), hcount(op.basis_p), H, op.p2m_basis.get(),
+                                           op.cl_panel.get(), x, M, op.p2m_part.get());
+    if (red.n) k_p2m_reduce<<<red.n, 128, 0, s>>>(red.d.get(), H, op.p2m_part.get(), M);
+  } else {
+    if (!leaves) {
+      leaves = S.leaves.get();
+      n_leaves = S.n_leaves;
+    }
+    if (n_leaves <= 0) return;
+    if (C == 1)
     k_p2m_basis<1><<<n_leaves, 256, 0, s>>>(leaves, S.body_start.get(), S.body_count.get(),
                                               S.n_points, H, op.basis_kind_for_sys,
                                               op.p2m_basis.get(), op.s_panel.get(), x, S.px.get(),
@@ -220,6 +332,7 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
                                               S.n_points, H, op.basis_kind_for_sys,
                                               op.p2m_basis.get(), op.s_panel.get(), x, S.px.get(),
                                               S.py.get(), S.pz.get(), M);
+  }
   FMM_LAUNCH_CHECK();
 }
 

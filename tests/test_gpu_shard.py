@@ -60,7 +60,8 @@ def test_nccl_world1_shard_matches_and_solves():
     ref = op.apply(x, 12)
     tb, sb = leaf_bounds(op, 1)
     op.shard(0, 1, tb, sb, nccl_unique_id())
-    np.testing.assert_array_equal(op.apply(x, 12), ref)
+    # the sharded upward pass is P2M + M2M (the unsharded one direct): equal to roundoff
+    assert rel_l2(op.apply(x, 12), ref) <= 1e-13
     res = solve(op, g["rhs"], eta=cfg.tol, p_initial=cfg.p_initial, p_min=cfg.p_min)
     assert res.orders == g["relaxed_orders"].tolist()
     assert rel_l2(res.x, g["relaxed_x"]) <= 1e-6
