@@ -25,10 +25,10 @@ constexpr int P2P_THREADS = 256;
 
 template <P2PKind K>
 struct P2PTraits;
-template <> struct P2PTraits<P2PKind::LAP_Q> { static constexpr int NW = 1, NC = 1; };
-template <> struct P2PTraits<P2PKind::LAP_D> { static constexpr int NW = 3, NC = 1; };
-template <> struct P2PTraits<P2PKind::STOKESLET> { static constexpr int NW = 3, NC = 3; };
-template <> struct P2PTraits<P2PKind::STRESSLET> { static constexpr int NW = 6, NC = 3; };
+template <> struct P2PTraits<P2PKind::LAP_Q> { static constexpr int NW = 1, NC = 1, TPT = 2; };
+template <> struct P2PTraits<P2PKind::LAP_D> { static constexpr int NW = 3, NC = 1, TPT = 4; };
+template <> struct P2PTraits<P2PKind::STOKESLET> { static constexpr int NW = 3, NC = 3, TPT = 2; };
+template <> struct P2PTraits<P2PKind::STRESSLET> { static constexpr int NW = 6, NC = 3, TPT = 2; };
 
 // 1/sqrt(x) for x > 0 to ~1 ulp: the SFU's double-precision seed (MUFU.RSQ64H,
 // ~2^-22) plus one third-order Newton step, y (1 + e/2 + 3e^2/8), e = 1 - x y^2:
@@ -41,9 +41,27 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
+// Second-order Newton step on the same seed, y (1 + (1 - x y^2) / 2): relative
+// error ~1.5 (2^-22.9)^2 ~ 3e-14, used by the double layer (4 DP instructions).
+__device__ __forceinline__ double rsqrt_nr2(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return fma(y, fma(-0.5 * x * y, y, 0.5), y);
+}
+
 template <P2PKind K>
 __device__ __forceinline__ void interact(double rx, double ry, double rz, const double* wv,
                                          double* acc) {
+  if (K == P2PKind::LAP_D) {
+    // d2 + 1e-200: a coincident pair (r = 0) gives r.n = 0 times a finite
+    // 1e300 instead of the masked branch; for any other pair the bias is far
+    // below one ulp of d2.
+    const double d2 = fma(rx, rx, fma(ry, ry, fma(rz, rz, 1e-200)));
+    const double inv = rsqrt_nr2(d2);
+    const double rn = fma(rx, wv[0], fma(ry, wv[1], rz * wv[2]));
+    acc[0] = fma(rn, inv * inv * inv, acc[0]);
+    return;
+  }
   const double d2 = fma(rx, rx, fma(ry, ry, rz * rz));
   const double inv = d2 > 0.0 ? rsqrt_nr(d2) : 0.0;
   if (K == P2PKind::LAP_Q) {
@@ -79,7 +97,7 @@ k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __rest
       int max_src, const double* __restrict__ w, double* __restrict__ part) {
   constexpr int NW = P2PTraits<K>::NW, NC = P2PTraits<K>::NC;
   constexpr int NPL = SrcPlanes<NW>::N;
-  constexpr int TPT = 2;  // targets per thread: every staged source is used twice
+  constexpr int TPT = P2PTraits<K>::TPT;  // targets per thread: each staged source is reused TPT times
   extern __shared__ double2 sh2[];
   const P2PItem it = items[blockIdx.x];
   int ns = 0;
@@ -160,9 +178,9 @@ template <P2PKind K>
 void launch_p2p_t(const TreeDev& S, const TreeDev& T, const P2PItem* items, int n_items,
                   const int* p2p_src, int max_src, const double* w, double* part, cudaStream_t st) {
   constexpr int NPL = SrcPlanes<P2PTraits<K>::NW>::N;
-  // shared memory: the staged sources, or the group reduction (256 * 2 targets * 3 comps)
+  // shared memory: the staged sources, or the group reduction (threads * TPT * comps)
   const size_t smem = std::max((size_t)max_src * NPL * sizeof(double2),
-                               (size_t)P2P_THREADS * 2 * 3 * sizeof(double));
+                               (size_t)P2P_THREADS * P2PTraits<K>::TPT * P2PTraits<K>::NC * sizeof(double));
   FMM_REQUIRE(smem <= 227 * 1024, "P2P: source slice too large for shared memory");
   FMM_CUDA(cudaFuncSetAttribute(k_p2p<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (n_items) k_p2p<K><<<n_items, P2P_THREADS, smem, st>>>(S, T, items, p2p_src, max_src, w, part);
