@@ -13,10 +13,11 @@
 
 namespace fmmbem {
 
+// (m0, mstep): only the columns m = m0, m0 + mstep, ... (split over threads)
 template <int C, bool GRAD>
 __device__ __forceinline__ void l2p_eval(const double2* __restrict__ L, int H, int p, double x,
                                          double y, double z, double* pot, double* grad,
-                                         const double* __restrict__ rec) {
+                                         const double* __restrict__ rec, int m0 = 0, int mstep = 1) {
   const double rho2 = x * x + y * y + z * z;
   double zr[C], zi[C], gz[C];
 #pragma unroll
@@ -24,6 +25,7 @@ __device__ __forceinline__ void l2p_eval(const double2* __restrict__ L, int H, i
   double2 diag = make_double2(1.0, 0.0);
   for (int m = 0; m <= p; ++m) {
     if (m > 0) diag = cscale(cmul(make_double2(x, y), diag), __ldg(rec + REC_DIAG + m));
+    if (m < m0 || (m - m0) % mstep) continue;
     double2 prev2 = make_double2(0.0, 0.0), cur = diag;
     const double w = m == 0 ? 1.0 : 2.0;
     for (int n = m; n <= p; ++n) {

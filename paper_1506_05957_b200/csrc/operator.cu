@@ -90,6 +90,8 @@ struct EpiArgs {
   const P2PItem* items;
   const double* part;
   const double2* L;
+  const int* path_off;  // per target cell: the cells whose local expansions reach its targets
+  const int* path;
   int p;
   const int* rowptr;
   const int* cols;
@@ -101,45 +103,78 @@ struct EpiArgs {
   int tbody_a;
 };
 
+// NS threads per target (NS > 1 for the one-channel kinds): slice k takes the
+// L2P columns m = k mod NS, every NS-th near-field item and correction entry;
+// the slices' partials are added in slice order.
+template <int KIND> constexpr int epi_slices() { return EpiTraits<KIND>::C == 1 ? 4 : 1; }
+constexpr int EPI_TGT = 128;  // targets per pass
+
 template <int KIND, bool FAR>
-__global__ void __launch_bounds__(128) k_epilogue(TreeDev T, EpiArgs a) {
+__global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeDev T, EpiArgs a) {
   using Tr = EpiTraits<KIND>;
-  constexpr int C = Tr::C, NC = Tr::NC;
+  constexpr int C = Tr::C, NC = Tr::NC, NS = epi_slices<KIND>();
   extern __shared__ double2 sL[];
+  double* red = reinterpret_cast<double*>(sL + (FAR ? C * hcount(a.p) : 0));  // [NS][EPI_TGT][2]
   const int li = blockIdx.x;
   const int leaf = a.leaves[li];
   const int H = hcount(a.p);
-  if (FAR) {
-    for (int i = threadIdx.x; i < C * H; i += blockDim.x) sL[i] = a.L[(size_t)leaf * C * H + i];
-    __syncthreads();
-  }
   const int t0 = T.body_start[leaf], nt = T.body_count[leaf];
-  const double cx = T.cx[leaf], cy = T.cy[leaf], cz = T.cz[leaf];
   const int ib = a.item_begin[li], ie = a.item_begin[li + 1];
-  for (int lt = threadIdx.x; lt < nt; lt += blockDim.x) {
-    const int ti = t0 + lt;
+  const int tl = threadIdx.x % EPI_TGT, slice = threadIdx.x / EPI_TGT;
+  for (int base = 0; base < nt; base += EPI_TGT) {
+    const int lt = base + tl;
+    const bool valid = lt < nt;
+    const int ti = t0 + (valid ? lt : 0);
+    double pot[C], grad[3 * C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) { pot[c] = 0.0; grad[3 * c] = grad[3 * c + 1] = grad[3 * c + 2] = 0.0; }
+    if (FAR) {
+      // each path cell's local expansion (the leaf, then its ancestors with M2L terms)
+      for (int k = a.path_off[leaf]; k < a.path_off[leaf + 1]; ++k) {
+        const int cell = a.path[k];
+        __syncthreads();
+        for (int i = threadIdx.x; i < C * H; i += blockDim.x) sL[i] = a.L[(size_t)cell * C * H + i];
+        __syncthreads();
+        if (valid)
+          l2p_eval<C, Tr::GRAD>(sL, H, a.p, T.px[ti] - T.cx[cell], T.py[ti] - T.cy[cell],
+                                T.pz[ti] - T.cz[cell], pot, grad, T.rec, slice, NS);
+      }
+    }
     const int pn = T.perm[ti];
     double near[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) near[c] = 0.0;
-    for (int it = ib; it < ie; ++it) {
-      const double* pp = a.part + (size_t)(a.items[it].out_off + lt) * NC;
+    if (valid)
+      for (int it = ib + slice; it < ie; it += NS) {
+        const double* pp = a.part + (size_t)(a.items[it].out_off + lt) * NC;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) near[c] += pp[c];
-    }
-    const double tx = T.px[ti], ty = T.py[ti], tz = T.pz[ti];
-    double pot[C], grad[3 * C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) { pot[c] = 0.0; grad[3 * c] = grad[3 * c + 1] = grad[3 * c + 2] = 0.0; }
-    if (FAR) l2p_eval<C, Tr::GRAD>(sL, H, a.p, tx - cx, ty - cy, tz - cz, pot, grad, T.rec);
+        for (int c = 0; c < NC; ++c) near[c] += pp[c];
+      }
     if (KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) {
       double corr = 0.0;
-      for (int e = a.rowptr[pn]; e < a.rowptr[pn + 1]; ++e) corr = fma(a.vals[e], a.x[a.cols[e]], corr);
-      const double layer = (pot[0] + near[0]) / FOUR_PI + corr;
-      const double v = a.alpha * a.x[pn] + a.beta * layer;
-      if (a.ysorted) a.ysorted[ti - a.tbody_a] = v;
-      else a.y[pn] = v;
-    } else {
+      if (valid)
+        for (int e = a.rowptr[pn] + slice; e < a.rowptr[pn + 1]; e += NS)
+          corr = fma(a.vals[e], a.x[a.cols[e]], corr);
+      double far_near = pot[0] + near[0];
+      if (NS > 1) {
+        red[(slice * EPI_TGT + tl) * 2] = far_near;
+        red[(slice * EPI_TGT + tl) * 2 + 1] = corr;
+        __syncthreads();
+        if (slice == 0)
+          for (int k = 1; k < NS; ++k) {
+            far_near += red[(k * EPI_TGT + tl) * 2];
+            corr += red[(k * EPI_TGT + tl) * 2 + 1];
+          }
+        __syncthreads();
+      }
+      if (slice == 0 && valid) {
+        const double layer = far_near / FOUR_PI + corr;
+        const double v = a.alpha * a.x[pn] + a.beta * layer;
+        if (a.ysorted) a.ysorted[ti - a.tbody_a] = v;
+        else a.y[pn] = v;
+      }
+    } else if (valid) {
+      const double tx = T.px[ti], ty = T.py[ti], tz = T.pz[ti];
       const double xt[3] = {tx, ty, tz};
       double u[3];
       for (int i = 0; i < 3; ++i) {
@@ -183,15 +218,16 @@ void launch_density(BemOp& op, const double* x, cudaStream_t s) {
 
 template <int KIND>
 void launch_epilogue(BemOp& op, const EpiArgs& a, bool far, cudaStream_t s, int nl) {
-  constexpr int C = EpiTraits<KIND>::C;
-  const size_t smem = far ? (size_t)C * hcount(a.p) * sizeof(double2) : 0;
+  constexpr int C = EpiTraits<KIND>::C, NS = epi_slices<KIND>();
+  const size_t red = NS > 1 ? (size_t)NS * EPI_TGT * 2 * sizeof(double) : 0;
+  const size_t smem = (far ? (size_t)C * hcount(a.p) * sizeof(double2) : 0) + red;
   if (nl <= 0) return;
   if (far) {
     FMM_CUDA(cudaFuncSetAttribute(k_epilogue<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(C * hcount(P_MAX) * sizeof(double2))));
-    k_epilogue<KIND, true><<<nl, 128, smem, s>>>(tree_dev(op.plan.tgt), a);
+                                  (int)(C * hcount(P_MAX) * sizeof(double2) + red)));
+    k_epilogue<KIND, true><<<nl, EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
   } else {
-    k_epilogue<KIND, false><<<nl, 128, 0, s>>>(tree_dev(op.plan.tgt), a);
+    k_epilogue<KIND, false><<<nl, EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
   }
   FMM_LAUNCH_CHECK();
 }
@@ -391,11 +427,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     else
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);
-    record(op, ST_DOWN, false, s);
-    if (sharded)
-      launch_l2l(pl.tgt, sw.l2l_off, sw.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
-    else
-      launch_l2l(pl.tgt, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
+    record(op, ST_DOWN, false, s);  // (no L2L levels: the epilogue walks each leaf's path)
     record(op, ST_DOWN, true, s);
   }
   FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
@@ -408,6 +440,8 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   const int n_epi = sharded ? sw.n_epi_leaves : pl.tgt.n_leaves;
   a.part = c.dense ? op.part_dense.get() : op.part.get();
   a.L = op.L.get();
+  a.path_off = pl.epi_path_off.get();
+  a.path = pl.epi_path.get();
   a.p = c.p;
   a.rowptr = op.near_rowptr.get();
   a.cols = op.near_cols.get();

@@ -98,6 +98,11 @@ struct Plan {
 
   // pruned vertical passes: M2M only for parents whose multipole is needed by an
   // M2L (or an ancestor's), L2L only below cells that carry a local expansion
+  // direct downward pass: per target leaf, the cells on its path to the root
+  // (itself first) that receive M2L terms; the epilogue evaluates each one's
+  // local expansion at the targets (L2L is exact, so this equals the L2L chain)
+  DevBuf<int> epi_path_off;  // n_tgt_cells + 1 (empty for non-leaves)
+  DevBuf<int> epi_path;
   std::vector<int> m2m_level_off, l2l_level_off;
   DevBuf<int> m2m_cells, l2l_cells;
   // octant-grouped M2M: items (rtab id, begin, end) into m2m_gchild, per parent level

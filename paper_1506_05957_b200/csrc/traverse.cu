@@ -379,6 +379,16 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
       plan.l2l_level_off.push_back((int)cells.size());
     }
     plan.l2l_cells.upload(cells.empty() ? std::vector<int>(1, 0) : cells, s);
+    std::vector<int> poff(T.n_cells + 1, 0), path;
+    for (int c = 0; c < T.n_cells; ++c) {
+      poff[c] = (int)path.size();
+      if (T.h_n_child[c] != 0) continue;
+      for (int a = c; a >= 0; a = T.h_parent[a])
+        if (plan.h_m2l_row[a + 1] > plan.h_m2l_row[a]) path.push_back(a);
+    }
+    poff[T.n_cells] = (int)path.size();
+    plan.epi_path_off.upload(poff, s);
+    plan.epi_path.upload(path.empty() ? std::vector<int>(1, 0) : path, s);
   }
   for (Tree* tr : {&plan.src, &plan.tgt}) {
     std::vector<int> rt(tr->n_cells, 0);
