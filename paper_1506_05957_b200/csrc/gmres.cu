@@ -9,6 +9,8 @@
 // read-back per iteration, which is also the only host synchronisation.
 // Reductions are two-level with a fixed combination order (bitwise
 // reproducible from run to run).
+#include <cooperative_groups.h>
+
 #include <cmath>
 
 #include "operator.cuh"
@@ -111,6 +113,52 @@ __global__ void k_scale(int64_t n, const double* b, const double* nb, double* v)
     v[i] = b[i] / d;
 }
 
+// One Arnoldi step in a single cooperative launch (grid-wide barriers between
+// the MGS sweeps): for j = 0..k, w -= h_{j-1} v_{j-1} fused with h_j = v_j . w;
+// then w -= h_k v_k, h_{k+1} = ||w||, v_{k+1} = w / h_{k+1}.  Block partials
+// are written per sweep and every block adds them in the same fixed order,
+// so all blocks hold bitwise the same h_j.
+constexpr int AB = 148;  // blocks (one per SM)
+
+__device__ double grid_total(double part, double* partials, double* sh) {
+  namespace cg = cooperative_groups;
+  if (threadIdx.x == 0) partials[blockIdx.x] = part;
+  cg::this_grid().sync();
+  double t = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) t += __ldcg(partials + b);
+  t = block_sum(t, sh);
+  __shared__ double bc;
+  if (threadIdx.x == 0) bc = t;
+  __syncthreads();
+  return bc;
+}
+
+__global__ void __launch_bounds__(RT) k_arnoldi(int64_t n, int k, const double* __restrict__ V,
+                                                double* w, double* partials, double* hd) {
+  __shared__ double sh[RT / 32];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double h = 0.0;
+  for (int j = 0; j <= k + 1; ++j) {
+    const double* vprev = j ? V + (size_t)(j - 1) * n : nullptr;
+    const double* v = j <= k ? V + (size_t)j * n : nullptr;
+    double acc = 0.0;
+    for (int64_t i = i0; i < n; i += stride) {
+      double wi = w[i];
+      if (vprev) {
+        wi = wi - h * vprev[i];
+        w[i] = wi;
+      }
+      acc = v ? fma(v[i], wi, acc) : fma(wi, wi, acc);
+    }
+    // alternate two partial arrays so a fast block cannot overwrite a slow block's read
+    h = grid_total(block_sum(acc, sh), partials + (j & 1) * gridDim.x, sh);
+    if (j > k) h = sqrt(h);
+    if (i0 == 0) hd[j] = h;
+  }
+  for (int64_t i = i0; i < n; i += stride) w[i] = h > 0.0 ? w[i] / h : 0.0;
+}
+
 double relax_eps(double r, double eta) { return std::min(eta / std::min(std::max(r, eta), 1.0), 1.0); }
 
 int schedule_p(double r, double eta, int p_initial, int p_min) {
@@ -135,7 +183,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   DevBuf<double>& partials = op.g_partials;
   DevBuf<double>& scal = op.g_scal;
   DevBuf<unsigned>& counter = op.g_counter;
-  partials.ensure(RB);
+  partials.ensure(std::max(RB, 2 * AB));
   scal.ensure(max_iter + 3);
   if (!counter.size()) {
     counter.ensure(1);
@@ -171,13 +219,16 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     prev_p = p;
     double* w = V.get() + (size_t)(k + 1) * n;
     op_apply_device(op, V.get() + (size_t)k * n, w, p);
-    for (int j = 0; j <= k; ++j)
-      k_mgs<<<RB, RT, 0, s>>>(n, V.get() + (size_t)j * n, w, j ? V.get() + (size_t)(j - 1) * n : nullptr,
-                              j ? hd + j - 1 : nullptr, partials.get(), counter.get(), hd + j);
-    k_norm<<<RB, RT, 0, s>>>(n, w, V.get() + (size_t)k * n, hd + k, partials.get(), counter.get(), hd + k + 1);
-    k_normalize<<<RB, RT, 0, s>>>(n, w, hd + k + 1);
+    {
+      const double* Vc = V.get();
+      double* pp = partials.get();
+      int kk = k;
+      int64_t nn = n;
+      void* args[] = {&nn, &kk, &Vc, &w, &pp, &hd};
+      FMM_CUDA(cudaLaunchCooperativeKernel((const void*)k_arnoldi, dim3(AB), dim3(RT), args, 0, s));
+    }
     FMM_LAUNCH_CHECK();
-    op.kernel_launches += k + 3;
+    op.kernel_launches += 1;
     FMM_CUDA(cudaMemcpyAsync(hcol.data(), hd, (k + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
     FMM_CUDA(cudaStreamSynchronize(s));
     op_collect_stage_times(op);
