@@ -92,7 +92,7 @@ __device__ __forceinline__ void interact(double rx, double ry, double rz, const 
 template <int NW> struct SrcPlanes { static constexpr int N = (3 + NW + 1) / 2; };
 
 template <P2PKind K>
-__global__ void __launch_bounds__(P2P_THREADS)
+__global__ void __launch_bounds__(P2P_THREADS, 4)
 k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __restrict__ p2p_src,
       int max_src, const double* __restrict__ w, double* __restrict__ part) {
   constexpr int NW = P2PTraits<K>::NW, NC = P2PTraits<K>::NC;
