@@ -60,9 +60,10 @@ inline int p2p_comps(P2PKind k) { return (k == P2PKind::LAP_Q || k == P2PKind::L
 // Writes per-item partial sums part[(item.out_off + local_target) * comps + comp].
 // Source strengths (sorted source order): LAP_Q: w[ns]; LAP_D: w[ns*3] dipoles;
 // STOKESLET: w[ns*3] forces; STRESSLET: w[ns*6] = (force, normal).
+// CTA b takes item order[b] (largest work first), or item b when order is null.
 void launch_p2p(P2PKind kind, const TreeDev& S, const TreeDev& T, const P2PItem* items,
                 int n_items, const int* p2p_src, int max_sources, const double* w, double* part,
-                cudaStream_t st);
+                cudaStream_t st, const int* order);
 
 // generic channel near field (FmmPlan.near_field): charges q[C][ns] and/or dipoles d[C][ns][3];
 // accumulates into pot[C][nt] (+ grad[C][nt][3]) in ORIGINAL target order.

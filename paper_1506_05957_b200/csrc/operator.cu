@@ -390,13 +390,14 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   record(op, ST_P2P, false, op.s_near);
   if (c.dense)
     launch_p2p((P2PKind)c.kind, S, T, op.dense_items.get(), (int)op.dense_items_h.size(),
-               op.dense_src.get(), op.dense_max_sources, w, op.part_dense.get(), op.s_near);
+               op.dense_src.get(), op.dense_max_sources, w, op.part_dense.get(), op.s_near,
+               nullptr);
   else if (sharded)
     launch_p2p((P2PKind)c.kind, S, T, sw.items.get(), (int)sw.items_h.size(), pl.p2p_src.get(),
-               sw.max_item_sources, w, op.part.get(), op.s_near);
+               sw.max_item_sources, w, op.part.get(), op.s_near, sw.p2p_order.get());
   else
     launch_p2p((P2PKind)c.kind, S, T, pl.d_items.get(), (int)pl.items.size(), pl.p2p_src.get(),
-               op.max_item_sources, w, op.part.get(), op.s_near);
+               op.max_item_sources, w, op.part.get(), op.s_near, pl.p2p_order.get());
   record(op, ST_P2P, true, op.s_near);
   FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
   // far field on the main stream

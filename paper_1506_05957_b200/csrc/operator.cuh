@@ -33,6 +33,7 @@ struct ShardWork {
   int n_epi_leaves = 0;
   std::vector<P2PItem> items_h;
   DevBuf<P2PItem> items;
+  DevBuf<int> p2p_order;
   DevBuf<int> item_begin;
   int64_t part_len = 0;
   int max_item_sources = 0;

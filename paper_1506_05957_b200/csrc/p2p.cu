@@ -93,13 +93,14 @@ template <int NW> struct SrcPlanes { static constexpr int N = (3 + NW + 1) / 2; 
 
 template <P2PKind K>
 __global__ void __launch_bounds__(P2P_THREADS, 4)
-k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __restrict__ p2p_src,
+k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __restrict__ order,
+      const int* __restrict__ p2p_src,
       int max_src, const double* __restrict__ w, double* __restrict__ part) {
   constexpr int NW = P2PTraits<K>::NW, NC = P2PTraits<K>::NC;
   constexpr int NPL = SrcPlanes<NW>::N;
   constexpr int TPT = P2PTraits<K>::TPT;  // targets per thread: each staged source is reused TPT times
   extern __shared__ double2 sh2[];
-  const P2PItem it = items[blockIdx.x];
+  const P2PItem it = items[order ? order[blockIdx.x] : (int)blockIdx.x];
   int ns = 0;
   for (int k = it.pair_begin; k < it.pair_end; ++k) {
     const int leaf = p2p_src[k];
@@ -176,26 +177,28 @@ k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __rest
 
 template <P2PKind K>
 void launch_p2p_t(const TreeDev& S, const TreeDev& T, const P2PItem* items, int n_items,
-                  const int* p2p_src, int max_src, const double* w, double* part, cudaStream_t st) {
+                  const int* p2p_src, int max_src, const double* w, double* part, cudaStream_t st,
+                  const int* order) {
   constexpr int NPL = SrcPlanes<P2PTraits<K>::NW>::N;
   // shared memory: the staged sources, or the group reduction (threads * TPT * comps)
   const size_t smem = std::max((size_t)max_src * NPL * sizeof(double2),
                                (size_t)P2P_THREADS * P2PTraits<K>::TPT * P2PTraits<K>::NC * sizeof(double));
   FMM_REQUIRE(smem <= 227 * 1024, "P2P: source slice too large for shared memory");
   FMM_CUDA(cudaFuncSetAttribute(k_p2p<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (n_items) k_p2p<K><<<n_items, P2P_THREADS, smem, st>>>(S, T, items, p2p_src, max_src, w, part);
+  if (n_items)
+    k_p2p<K><<<n_items, P2P_THREADS, smem, st>>>(S, T, items, order, p2p_src, max_src, w, part);
   FMM_LAUNCH_CHECK();
 }
 
 void launch_p2p(P2PKind kind, const TreeDev& S, const TreeDev& T, const P2PItem* items,
                 int n_items, const int* p2p_src, int max_sources, const double* w, double* part,
-                cudaStream_t st) {
+                cudaStream_t st, const int* order) {
   const int ms = std::max(max_sources, 1);
   switch (kind) {
-    case P2PKind::LAP_Q: return launch_p2p_t<P2PKind::LAP_Q>(S, T, items, n_items, p2p_src, ms, w, part, st);
-    case P2PKind::LAP_D: return launch_p2p_t<P2PKind::LAP_D>(S, T, items, n_items, p2p_src, ms, w, part, st);
-    case P2PKind::STOKESLET: return launch_p2p_t<P2PKind::STOKESLET>(S, T, items, n_items, p2p_src, ms, w, part, st);
-    case P2PKind::STRESSLET: return launch_p2p_t<P2PKind::STRESSLET>(S, T, items, n_items, p2p_src, ms, w, part, st);
+    case P2PKind::LAP_Q: return launch_p2p_t<P2PKind::LAP_Q>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
+    case P2PKind::LAP_D: return launch_p2p_t<P2PKind::LAP_D>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
+    case P2PKind::STOKESLET: return launch_p2p_t<P2PKind::STOKESLET>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
+    case P2PKind::STRESSLET: return launch_p2p_t<P2PKind::STRESSLET>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
   }
 }
 

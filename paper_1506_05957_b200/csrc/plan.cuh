@@ -92,6 +92,7 @@ struct Plan {
   std::vector<int> h_p2p_row, h_p2p_src;
   std::vector<P2PItem> items;
   DevBuf<P2PItem> d_items;
+  DevBuf<int> p2p_order;  // items by decreasing work (persistent P2P schedule)
   DevBuf<int> tleaf_item_begin;  // per target leaf index (body order) -> first item; n_leaves + 1
   int64_t part_len = 0;          // total targets over items
   int64_t p2p_interactions = 0;
@@ -121,6 +122,9 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
 // (re)build the irregular-harmonic tables for M2L up to order 2p
 void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s);
 void plan_ensure_rot(Plan& plan, int p, cudaStream_t s);
+// item indices by decreasing work (targets x sources), for the persistent P2P kernel
+std::vector<int> p2p_schedule(const Tree& T, const Tree& S, const std::vector<P2PItem>& items,
+                              const std::vector<int>& p2p_src);
 // dense "every source leaf for every target leaf" item list (dense_apply)
 void plan_dense_items(const Plan& plan, std::vector<P2PItem>& items, std::vector<int>& row,
                       std::vector<int>& src, std::vector<int>& item_begin, int64_t& part_len);

@@ -193,6 +193,10 @@ void op_shard_setup(BemOp& op, int rank, int world, const int* tb, const int* sb
   }
   ib[own.size()] = (int)sw.items_h.size();
   sw.items.upload(sw.items_h.empty() ? std::vector<P2PItem>(1) : sw.items_h, s);
+  {
+    const std::vector<int> ord = p2p_schedule(op.plan.tgt, op.plan.src, sw.items_h, op.plan.h_p2p_src);
+    sw.p2p_order.upload(ord.empty() ? std::vector<int>(1, 0) : ord, s);
+  }
   sw.item_begin.upload(ib, s);
   op.part.ensure((size_t)std::max<int64_t>(std::max(sw.part_len, pl.part_len), 1) * 3);
   // needed target cells: ancestors-or-self of own leaves

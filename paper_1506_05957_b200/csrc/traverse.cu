@@ -197,6 +197,20 @@ void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s) {
   plan.igrid_p = p;
 }
 
+std::vector<int> p2p_schedule(const Tree& T, const Tree& S, const std::vector<P2PItem>& items,
+                              const std::vector<int>& p2p_src) {
+  std::vector<int64_t> cost(items.size());
+  for (size_t i = 0; i < items.size(); ++i) {
+    int64_t ns = 0;
+    for (int k = items[i].pair_begin; k < items[i].pair_end; ++k) ns += S.h_body_count[p2p_src[k]];
+    cost[i] = ns * T.h_body_count[items[i].tgt_leaf];
+  }
+  std::vector<int> ord(items.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  return ord;
+}
+
 void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
   FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
   if (plan.rot_p >= p) return;
@@ -324,6 +338,10 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
   plan_make_items(T, S, plan.h_p2p_row, plan.h_p2p_src, 512, plan.items, item_begin,
                   plan.part_len, plan.p2p_interactions);
   plan.d_items.upload(plan.items, s);
+  {
+    const std::vector<int> ord = p2p_schedule(T, S, plan.items, plan.h_p2p_src);
+    plan.p2p_order.upload(ord.empty() ? std::vector<int>(1, 0) : ord, s);
+  }
   plan.tleaf_item_begin.upload(item_begin, s);
 
   // needed(c): c is an M2L source or its parent's multipole is needed
