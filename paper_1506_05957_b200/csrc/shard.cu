@@ -5,7 +5,7 @@
 // balanced by work) and of source leaves (balanced by bodies):
 //   1. P2M of its own source leaves, NCCL all-gather of the leaf multipoles
 //      (equal-size padded slices), then the (cheap) M2M on every rank;
-//   2. M2L / L2L only for target cells that are ancestors-or-self of its
+//   2. M2L only for target cells that are ancestors-or-self of its
 //      leaves, P2P items and epilogue only for its leaves -> its y entries;
 //   3. NCCL all-gather of the y slices, scattered back to panel order.
 // The Krylov vectors stay replicated, so GMRES (and the relaxed-p decisions)
