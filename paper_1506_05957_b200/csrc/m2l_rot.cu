@@ -192,7 +192,8 @@ __global__ void k_rot_aux(const double* __restrict__ geo, int n_off, int P, doub
 template <int P>
 __global__ void __launch_bounds__(ROT_WARPS * 32)
 k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ gpair,
-          const int* __restrict__ pair_src, const double* __restrict__ frag, int ttot,
+          const int* __restrict__ pair_src, const double* __restrict__ frag,
+          const int* __restrict__ dir, int ttot,
           const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
           double2* __restrict__ pout) {
   constexpr int H = hcount(P);
@@ -219,7 +220,7 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
     for (int i = lane; i <= 2 * P; i += 32) zz[i] = A[2 * (aux_p + 1) + i];
   }
   const int fr = lane >> 2, fc = lane & 3;  // fragment row / column-in-k
-  const double* T = frag + (size_t)u * 4 * ttot * 32 + lane;
+  const double* T = frag + (size_t)dir[u] * 4 * ttot * 32 + lane;
   auto load = [&](Frag& f, int tab, int n) {
     const int mt = frag_mt(n), ks = frag_ks(n);
     const double* tr = T + (size_t)(tab * ttot + frag_base(n)) * 32;
@@ -410,7 +411,8 @@ void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_
   }
   const int64_t units = (int64_t)n_items * C;
   k_m2l_rot<P><<<(unsigned)((units + ROT_WARPS - 1) / ROT_WARPS), ROT_WARPS * 32, smem, st>>>(
-      gitems, n_items, gpair, plan.m2l_src.get(), plan.rotf.get(), frag_base(plan.rot_p + 1),
+      gitems, n_items, gpair, plan.m2l_src.get(), plan.rotf.get(), plan.rot_dir.get(),
+      frag_base(plan.rot_p + 1),
       plan.rot_aux.get(), plan.rot_p, M, C, pout);
   FMM_LAUNCH_CHECK();
 }

@@ -504,7 +504,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
                                           op.x_in.get(), op.y_out.get(), op.m2l_part.get(),
                                           op.p2m_basis.get(), op.m2m_cout.get(), op.plan.rotf.get(),
-                                          op.plan.rot_aux.get(), op.cl_panel.get(),
+                                          op.plan.rot_aux.get(), op.plan.rot_dir.get(), op.cl_panel.get(),
                                           op.p2m_items.d.get(), op.p2m_reduce.d.get(), op.p2m_part.get()};
     if (sig != op.graph_sig) {
       clear_graphs(op);

@@ -68,7 +68,12 @@ struct Plan {
   int igrid_p = -1;        // I tables hold orders up to 2 * igrid_p
   // rotation-based M2L (m2l_rot.cu): per offset the scaled Wigner matrices a^n, n <= rot_p,
   // and (|D|, theta, phi)
+  // The a^n depend on the polar angle of D only: offsets with bitwise-equal
+  // cos(theta) share one table (rot_dir maps offset -> table).
   DevBuf<double> rot, rot_geo;
+  DevBuf<int> rot_dir;
+  int n_rot_dirs = 0;
+  std::vector<double> h_off;  // 3 * n_offsets
   DevBuf<double> rot_aux;  // per offset e^{-ik phi} and N!/|D|^(N+1)
   DevBuf<double> rotf;  // the same operators as DMMA 8x4 row fragments (m2l_rot.cu)
   int rot_p = -1;

@@ -214,11 +214,35 @@ std::vector<int> p2p_schedule(const Tree& T, const Tree& S, const std::vector<P2
 void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
   FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
   if (plan.rot_p >= p) return;
-  plan.rot.resize((size_t)std::max(plan.n_offsets, 1) * rot_table_size(p));
+  // one table per distinct polar angle (the offsets are lattice-exact, so equal
+  // directions give bitwise-equal z / |D|)
+  std::map<double, int> dirs;
+  std::vector<int> dir(plan.n_offsets);
+  std::vector<double> rep;
+  for (int u = 0; u < plan.n_offsets; ++u) {
+    const double x = plan.h_off[3 * u], y = plan.h_off[3 * u + 1], z = plan.h_off[3 * u + 2];
+    const double key = z / std::sqrt(x * x + y * y + z * z);
+    auto it = dirs.find(key);
+    if (it == dirs.end()) {
+      it = dirs.emplace(key, (int)dirs.size()).first;
+      rep.insert(rep.end(), {x, y, z});
+    }
+    dir[u] = it->second;
+  }
+  plan.n_rot_dirs = (int)dirs.size();
+  plan.rot_dir.upload(dir.empty() ? std::vector<int>(1, 0) : dir, s);
+  DevBuf<double> d_rep, geo_rep, one;
+  d_rep.upload(rep.empty() ? std::vector<double>(3, 1.0) : rep, s);
+  const int nd = std::max(plan.n_rot_dirs, 1);
+  plan.rot.resize((size_t)nd * rot_table_size(p));
+  geo_rep.resize((size_t)nd * 3);
+  compute_rot_tables(d_rep.get(), plan.n_rot_dirs, p, plan.rot.get(), geo_rep.get(), s);
+  // (|D|, theta, phi) of every offset (order-0 tables are a by-product)
   plan.rot_geo.resize((size_t)std::max(plan.n_offsets, 1) * 3);
-  compute_rot_tables(plan.off_d.get(), plan.n_offsets, p, plan.rot.get(), plan.rot_geo.get(), s);
-  plan.rotf.resize((size_t)std::max(plan.n_offsets, 1) * rot_frag_size(p));
-  build_rot_frag(plan.rot.get(), plan.n_offsets, p, plan.rotf.get(), s);
+  one.resize((size_t)std::max(plan.n_offsets, 1));
+  compute_rot_tables(plan.off_d.get(), plan.n_offsets, 0, one.get(), plan.rot_geo.get(), s);
+  plan.rotf.resize((size_t)nd * rot_frag_size(p));
+  build_rot_frag(plan.rot.get(), plan.n_rot_dirs, p, plan.rotf.get(), s);
   plan.rot_aux.resize((size_t)std::max(plan.n_offsets, 1) * rot_aux_size(p));
   build_rot_aux(plan.rot_geo.get(), plan.n_offsets, p, plan.rot_aux.get(), s);
   FMM_CUDA(cudaStreamSynchronize(s));
@@ -282,6 +306,7 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
   plan.m2l_src.upload(plan.h_m2l_src, s);
   plan.m2l_off.upload(offid, s);
   plan.off_d.upload(offd, s);
+  plan.h_off = offd;
   plan.m2l_tgt_cells.clear();
   for (int c = 0; c < T.n_cells; ++c)
     if (plan.h_m2l_row[c + 1] > plan.h_m2l_row[c]) plan.m2l_tgt_cells.push_back(c);
