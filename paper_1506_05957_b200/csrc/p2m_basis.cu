@@ -117,23 +117,49 @@ k_p2m_basis(const int* __restrict__ leaves, const int* __restrict__ body_start,
 // clustered entries (Laplace kinds, one channel), entry-major Bd[e][h]: work item
 // (cell, entry range, slot): acc[h] = sum_e Bd[e][h] x[panel(e)], one thread per h;
 // slot < 0 writes the cell's multipole, else a partial that k_p2m_reduce adds in order
+// 4 warps split the item's (<= 32) entries, lanes run over h (NJ = ceil(H/32)
+// per lane, every row load a coalesced 512 B), the warps' sums are added in
+// warp order through shared memory.
+constexpr int P2M_CHUNK = 32;
+
+template <int NJ>
 __global__ void __launch_bounds__(128)
 k_p2m_basis_cl(const int4* __restrict__ items, int Hp, int H, const double2* __restrict__ B,
                const int* __restrict__ e_panel, const double* __restrict__ x,
                double2* __restrict__ M, double2* __restrict__ part) {
+  __shared__ double sx[P2M_CHUNK];
+  __shared__ double2 red[4][NJ * 32];
   const int4 it = items[blockIdx.x];
-  double2* out = it.w < 0 ? M + (size_t)it.x * H : part + (size_t)it.w * H;
-  for (int h = threadIdx.x; h < H; h += blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
-    for (int e = it.y; e < it.z; ++e) {
-      const double s = __ldg(x + __ldg(e_panel + e));
-      const double2 v = __ldg(B + (size_t)e * Hp + h);
-      acc.x = fma(s, v.x, acc.x);
-      acc.y = fma(s, v.y, acc.y);
+  const int len = it.z - it.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < len) sx[threadIdx.x] = __ldg(x + __ldg(e_panel + it.y + threadIdx.x));
+  __syncthreads();
+  double2 acc[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) acc[j] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < P2M_CHUNK / 4; ++k) {
+    const int e = warp + 4 * k;
+    if (e < len) {
+      const double s = sx[e];
+      const double2* row = B + (size_t)(it.y + e) * Hp;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int h = lane + 32 * j;
+        if (h < H) {
+          const double2 v = __ldg(row + h);
+          acc[j].x = fma(s, v.x, acc[j].x);
+          acc[j].y = fma(s, v.y, acc[j].y);
+        }
+      }
     }
-    out[h] = acc;
   }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) red[warp][lane + 32 * j] = acc[j];
+  __syncthreads();
+  double2* out = it.w < 0 ? M + (size_t)it.x * H : part + (size_t)it.w * H;
+  for (int h = threadIdx.x; h < H; h += blockDim.x)
+    out[h] = cadd(cadd(cadd(red[0][h], red[1][h]), red[2][h]), red[3][h]);
 }
 
 // cells split over several items: (cell, first slot, slot count)
@@ -196,7 +222,6 @@ __global__ void k_basis_build_entries(int ne, int ptab, int kind, const int* __r
 // work items over the entries of the given cells, <= P2M_CHUNK entries each
 void set_p2m_items(BemOp& op, const std::vector<int>& cells, const std::vector<int>& range,
                    P2MItems& items, P2MItems& reduce, int& n_slots) {
-  constexpr int P2M_CHUNK = 32;
   std::vector<int4> it, red;
   int slot = 0;
   for (int c : cells) {
@@ -312,9 +337,19 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
     const P2MItems& red = direct ? op.p2m_reduce : op.p2m_leaf_reduce;
     FMM_REQUIRE(op.p2m_part.size() >= (size_t)std::max(op.n_p2m_slots, op.n_p2m_leaf_slots) * H,
                 "P2M partial buffer not sized");
-    if (it.n)
-      k_p2m_basis_cl<<<it.n, 128, 0, s>>>(it.d.get(), hcount(op.basis_p), H, op.p2m_basis.get(),
-                                           op.cl_panel.get(), x, M, op.p2m_part.get());
+    if (it.n) {
+      const int nj = (H + 31) / 32, Hp = hcount(op.basis_p);
+#define P2M_CL(NJ)                                                                              \
+  case NJ:                                                                                      \
+    k_p2m_basis_cl<NJ><<<it.n, 128, 0, s>>>(it.d.get(), Hp, H, op.p2m_basis.get(),              \
+                                            op.cl_panel.get(), x, M, op.p2m_part.get());        \
+    break;
+      switch (nj) {
+        P2M_CL(1) P2M_CL(2) P2M_CL(3) P2M_CL(4) P2M_CL(5) P2M_CL(6) P2M_CL(7) P2M_CL(8)
+        default: FMM_REQUIRE(false, "P2M: order out of range");
+      }
+#undef P2M_CL
+    }
     if (red.n) k_p2m_reduce<<<red.n, 128, 0, s>>>(red.d.get(), H, op.p2m_part.get(), M);
   } else {
     if (!leaves) {
