@@ -55,6 +55,8 @@ struct ShardWork {
 
 struct P2MItems {
   DevBuf<int4> d;
+  DevBuf<int> red_of;       // per item: its cell's reduce record, or -1
+  DevBuf<unsigned> arrive;  // per reduce record: items done (self-resetting)
   int n = 0;
 };
 

@@ -124,9 +124,10 @@ constexpr int P2M_CHUNK = 32;
 
 template <int NJ>
 __global__ void __launch_bounds__(128)
-k_p2m_basis_cl(const int4* __restrict__ items, int Hp, int H, const double2* __restrict__ B,
-               const int* __restrict__ e_panel, const double* __restrict__ x,
-               double2* __restrict__ M, double2* __restrict__ part) {
+k_p2m_basis_cl(const int4* __restrict__ items, const int* __restrict__ red_of,
+               const int4* __restrict__ reds, unsigned* arrive, int Hp, int H,
+               const double2* __restrict__ B, const int* __restrict__ e_panel,
+               const double* __restrict__ x, double2* __restrict__ M, double2* __restrict__ part) {
   __shared__ double sx[P2M_CHUNK];
   __shared__ double2 red[4][NJ * 32];
   const int4 it = items[blockIdx.x];
@@ -160,17 +161,23 @@ k_p2m_basis_cl(const int4* __restrict__ items, int Hp, int H, const double2* __r
   double2* out = it.w < 0 ? M + (size_t)it.x * H : part + (size_t)it.w * H;
   for (int h = threadIdx.x; h < H; h += blockDim.x)
     out[h] = cadd(cadd(cadd(red[0][h], red[1][h]), red[2][h]), red[3][h]);
-}
-
-// cells split over several items: (cell, first slot, slot count)
-__global__ void k_p2m_reduce(const int4* __restrict__ cells, int H, const double2* __restrict__ part,
-                             double2* __restrict__ M) {
-  const int4 c = cells[blockIdx.x];
+  if (it.w < 0) return;
+  // a cell split over several items: the last one to finish adds the partials in slot order
+  const int r = red_of[blockIdx.x];
+  const int4 rc = reds[r];
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(arrive + r, 1u) == (unsigned)rc.z - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
   for (int h = threadIdx.x; h < H; h += blockDim.x) {
-    double2 acc = part[(size_t)c.y * H + h];
-    for (int k = 1; k < c.z; ++k) acc = cadd(acc, part[(size_t)(c.y + k) * H + h]);
-    M[(size_t)c.x * H + h] = acc;
+    double2 acc = __ldcg(part + (size_t)rc.y * H + h);
+    for (int k = 1; k < rc.z; ++k) acc = cadd(acc, __ldcg(part + (size_t)(rc.y + k) * H + h));
+    M[(size_t)rc.x * H + h] = acc;
   }
+  if (threadIdx.x == 0) arrive[r] = 0u;
 }
 
 // Direct upward basis: entry e = (cell, cluster in the cell's subtree),
@@ -223,19 +230,26 @@ __global__ void k_basis_build_entries(int ne, int ptab, int kind, const int* __r
 void set_p2m_items(BemOp& op, const std::vector<int>& cells, const std::vector<int>& range,
                    P2MItems& items, P2MItems& reduce, int& n_slots) {
   std::vector<int4> it, red;
+  std::vector<int> red_of;
   int slot = 0;
   for (int c : cells) {
     const int e0 = range[2 * (size_t)c], e1 = range[2 * (size_t)c + 1], len = e1 - e0;
     const int nch = std::max(1, (len + P2M_CHUNK - 1) / P2M_CHUNK);
     if (nch == 1) {
       it.push_back(make_int4(c, e0, e1, -1));
+      red_of.push_back(-1);
       continue;
     }
     red.push_back(make_int4(c, slot, nch, 0));
-    for (int q = 0; q < nch; ++q)
+    for (int q = 0; q < nch; ++q) {
       it.push_back(make_int4(c, e0 + (int)((int64_t)len * q / nch), e0 + (int)((int64_t)len * (q + 1) / nch),
                              slot++));
+      red_of.push_back((int)red.size() - 1);
+    }
   }
+  items.red_of.upload(red_of.empty() ? std::vector<int>(1, -1) : red_of);
+  items.arrive.resize(std::max<size_t>(red.size(), 1));
+  items.arrive.zero();
   items.n = (int)it.size();
   items.d.upload(it.empty() ? std::vector<int4>(1) : it);
   reduce.n = (int)red.size();
@@ -341,7 +355,8 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
       const int nj = (H + 31) / 32, Hp = hcount(op.basis_p);
 #define P2M_CL(NJ)                                                                              \
   case NJ:                                                                                      \
-    k_p2m_basis_cl<NJ><<<it.n, 128, 0, s>>>(it.d.get(), Hp, H, op.p2m_basis.get(),              \
+    k_p2m_basis_cl<NJ><<<it.n, 128, 0, s>>>(it.d.get(), it.red_of.get(), red.d.get(),          \
+                                            it.arrive.get(), Hp, H, op.p2m_basis.get(),         \
                                             op.cl_panel.get(), x, M, op.p2m_part.get());        \
     break;
       switch (nj) {
@@ -350,7 +365,6 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
       }
 #undef P2M_CL
     }
-    if (red.n) k_p2m_reduce<<<red.n, 128, 0, s>>>(red.d.get(), H, op.p2m_part.get(), M);
   } else {
     if (!leaves) {
       leaves = S.leaves.get();
