@@ -92,6 +92,7 @@ struct EpiArgs {
   const double2* L;
   const int* path_off;  // per target cell: the cells whose local expansions reach its targets
   const int* path;
+  int max_path;
   int p;
   const int* rowptr;
   const int* cols;
@@ -113,34 +114,26 @@ template <int KIND, bool FAR>
 __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeDev T, EpiArgs a) {
   using Tr = EpiTraits<KIND>;
   constexpr int C = Tr::C, NC = Tr::NC, NS = epi_slices<KIND>();
-  extern __shared__ double2 sL[];
-  double* red = reinterpret_cast<double*>(sL + (FAR ? C * hcount(a.p) : 0));  // [NS][EPI_TGT][2]
+  extern __shared__ double2 sL[];  // [path cell][C][H], then the slice partials
   const int li = blockIdx.x;
   const int leaf = a.leaves[li];
   const int H = hcount(a.p);
+  const int pb = FAR ? a.path_off[leaf] : 0, np = FAR ? a.path_off[leaf + 1] - pb : 0;
+  double* red = reinterpret_cast<double*>(sL + (FAR ? (size_t)a.max_path * C * H : 0));  // [NS][EPI_TGT][2]
   const int t0 = T.body_start[leaf], nt = T.body_count[leaf];
   const int ib = a.item_begin[li], ie = a.item_begin[li + 1];
   const int tl = threadIdx.x % EPI_TGT, slice = threadIdx.x / EPI_TGT;
+  // every path cell's local expansion (the leaf, then its ancestors with M2L terms), staged once
+  for (int i = threadIdx.x; i < np * C * H; i += blockDim.x) {
+    const int k = i / (C * H), r = i - k * (C * H);
+    sL[i] = a.L[(size_t)a.path[pb + k] * C * H + r];
+  }
   for (int base = 0; base < nt; base += EPI_TGT) {
     const int lt = base + tl;
     const bool valid = lt < nt;
     const int ti = t0 + (valid ? lt : 0);
-    double pot[C], grad[3 * C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) { pot[c] = 0.0; grad[3 * c] = grad[3 * c + 1] = grad[3 * c + 2] = 0.0; }
-    if (FAR) {
-      // each path cell's local expansion (the leaf, then its ancestors with M2L terms)
-      for (int k = a.path_off[leaf]; k < a.path_off[leaf + 1]; ++k) {
-        const int cell = a.path[k];
-        __syncthreads();
-        for (int i = threadIdx.x; i < C * H; i += blockDim.x) sL[i] = a.L[(size_t)cell * C * H + i];
-        __syncthreads();
-        if (valid)
-          l2p_eval<C, Tr::GRAD>(sL, H, a.p, T.px[ti] - T.cx[cell], T.py[ti] - T.cy[cell],
-                                T.pz[ti] - T.cz[cell], pot, grad, T.rec, slice, NS);
-      }
-    }
     const int pn = T.perm[ti];
+    // near-field partials and the correction row first: their loads overlap the L2P below
     double near[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) near[c] = 0.0;
@@ -150,11 +143,27 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
 #pragma unroll
         for (int c = 0; c < NC; ++c) near[c] += pp[c];
       }
-    if (KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) {
-      double corr = 0.0;
+    double corr1 = 0.0;
+    if ((KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) && valid) {
+      const int e1 = a.rowptr[pn + 1];
+#pragma unroll 4
+      for (int e = a.rowptr[pn] + slice; e < e1; e += NS) corr1 = fma(a.vals[e], a.x[a.cols[e]], corr1);
+    }
+    double pot[C], grad[3 * C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) { pot[c] = 0.0; grad[3 * c] = grad[3 * c + 1] = grad[3 * c + 2] = 0.0; }
+    if (FAR) {
+      __syncthreads();  // (first pass: the staged expansions)
       if (valid)
-        for (int e = a.rowptr[pn] + slice; e < a.rowptr[pn + 1]; e += NS)
-          corr = fma(a.vals[e], a.x[a.cols[e]], corr);
+        for (int k = 0; k < np; ++k) {
+          const int cell = a.path[pb + k];
+          l2p_eval<C, Tr::GRAD>(sL + (size_t)k * C * H, H, a.p, T.px[ti] - T.cx[cell],
+                                T.py[ti] - T.cy[cell], T.pz[ti] - T.cz[cell], pot, grad, T.rec,
+                                slice, NS);
+        }
+    }
+    if (KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) {
+      double corr = corr1;
       double far_near = pot[0] + near[0];
       if (NS > 1) {
         red[(slice * EPI_TGT + tl) * 2] = far_near;
@@ -220,11 +229,14 @@ template <int KIND>
 void launch_epilogue(BemOp& op, const EpiArgs& a, bool far, cudaStream_t s, int nl) {
   constexpr int C = EpiTraits<KIND>::C, NS = epi_slices<KIND>();
   const size_t red = NS > 1 ? (size_t)NS * EPI_TGT * 2 * sizeof(double) : 0;
-  const size_t smem = (far ? (size_t)C * hcount(a.p) * sizeof(double2) : 0) + red;
+  const size_t lbytes = (size_t)std::max(a.max_path, 1) * C * sizeof(double2);
+  const size_t smem = (far ? lbytes * hcount(a.p) : 0) + red;
   if (nl <= 0) return;
   if (far) {
+    const size_t most = lbytes * hcount(P_MAX) + red;
+    FMM_REQUIRE(smem <= 227 * 1024, "epilogue: root paths too long for shared memory");
     FMM_CUDA(cudaFuncSetAttribute(k_epilogue<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(C * hcount(P_MAX) * sizeof(double2) + red)));
+                                  (int)std::min<size_t>(most, 227 * 1024)));
     k_epilogue<KIND, true><<<nl, EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
   } else {
     k_epilogue<KIND, false><<<nl, EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
@@ -443,6 +455,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   a.L = op.L.get();
   a.path_off = pl.epi_path_off.get();
   a.path = pl.epi_path.get();
+  a.max_path = pl.max_path;
   a.p = c.p;
   a.rowptr = op.near_rowptr.get();
   a.cols = op.near_cols.get();

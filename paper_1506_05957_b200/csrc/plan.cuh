@@ -109,6 +109,7 @@ struct Plan {
   // local expansion at the targets (L2L is exact, so this equals the L2L chain)
   DevBuf<int> epi_path_off;  // n_tgt_cells + 1 (empty for non-leaves)
   DevBuf<int> epi_path;
+  int max_path = 0;          // longest such list
   std::vector<int> m2m_level_off, l2l_level_off;
   DevBuf<int> m2m_cells, l2l_cells;
   // octant-grouped M2M: items (rtab id, begin, end) into m2m_gchild, per parent level

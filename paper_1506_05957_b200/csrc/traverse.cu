@@ -430,6 +430,8 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
         if (plan.h_m2l_row[a + 1] > plan.h_m2l_row[a]) path.push_back(a);
     }
     poff[T.n_cells] = (int)path.size();
+    plan.max_path = 0;
+    for (int c = 0; c < T.n_cells; ++c) plan.max_path = std::max(plan.max_path, poff[c + 1] - poff[c]);
     plan.epi_path_off.upload(poff, s);
     plan.epi_path.upload(path.empty() ? std::vector<int>(1, 0) : path, s);
   }
