@@ -39,6 +39,8 @@ struct Tree {
   const double* rec = nullptr;  // plan's reciprocal table (common.cuh)
 };
 
+constexpr int P2P_ITEM_SOURCES = 1024;  // sources per P2P work item (shared-memory tile)
+
 struct P2PItem {
   int tgt_leaf;   // target cell id
   int pair_begin; // range into p2p source-leaf list (CSR of the target leaf)
