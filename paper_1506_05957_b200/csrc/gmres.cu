@@ -35,7 +35,8 @@ __device__ double block_sum(double v, double* sh) {
 // finish: the last block to arrive adds the block partials (fixed assignment
 // of partials to threads and a fixed reduction tree: deterministic)
 __device__ void finish(double part, double* partials, unsigned* counter, double* out, bool do_sqrt,
-                       double* sh) {
+                       double* sh, double* mbox = nullptr, unsigned long long* mflag = nullptr,
+                       unsigned long long seq = 0) {
   __shared__ bool last;
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = part;
@@ -51,6 +52,11 @@ __device__ void finish(double part, double* partials, unsigned* counter, double*
   if (threadIdx.x == 0) {
     *out = do_sqrt ? sqrt(t) : t;
     *counter = 0u;
+    if (mflag) {
+      mbox[0] = *out;
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned long long*>(mflag) = seq;
+    }
   }
 }
 
@@ -75,7 +81,9 @@ __global__ void __launch_bounds__(RT) k_mgs(int64_t n, const double* __restrict_
 // w -= h * v; out = ||w||    (solver.py:102-103)
 __global__ void __launch_bounds__(RT) k_norm(int64_t n, double* w, const double* __restrict__ v,
                                              const double* hv, double* partials, unsigned* counter,
-                                             double* out) {
+                                             double* out, double* mbox = nullptr,
+                                             unsigned long long* mflag = nullptr,
+                                             unsigned long long seq = 0) {
   __shared__ double sh[RT / 32];
   const double h = v ? *hv : 0.0;
   double acc = 0.0;
@@ -87,7 +95,7 @@ __global__ void __launch_bounds__(RT) k_norm(int64_t n, double* w, const double*
     }
     acc = fma(wi, wi, acc);
   }
-  finish(block_sum(acc, sh), partials, counter, out, true, sh);
+  finish(block_sum(acc, sh), partials, counter, out, true, sh, mbox, mflag, seq);
 }
 
 // v = w / h (or zeros on breakdown)    (solver.py:104-107)
@@ -134,7 +142,8 @@ __device__ double grid_total(double part, double* partials, double* sh) {
 }
 
 __global__ void __launch_bounds__(RT) k_arnoldi(int64_t n, int k, const double* __restrict__ V,
-                                                double* w, double* partials, double* hd) {
+                                                double* w, double* partials, double* hd, double* mbox,
+                                                unsigned long long* mflag, unsigned long long seq) {
   __shared__ double sh[RT / 32];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -154,7 +163,14 @@ __global__ void __launch_bounds__(RT) k_arnoldi(int64_t n, int k, const double* 
     // alternate two partial arrays so a fast block cannot overwrite a slow block's read
     h = grid_total(block_sum(acc, sh), partials + (j & 1) * gridDim.x, sh);
     if (j > k) h = sqrt(h);
-    if (i0 == 0) hd[j] = h;
+    if (i0 == 0) {
+      hd[j] = h;
+      mbox[j] = h;
+    }
+  }
+  if (i0 == 0) {  // the column is complete: post it to the host
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(mflag) = seq;
   }
   for (int64_t i = i0; i < n; i += stride) w[i] = h > 0.0 ? w[i] / h : 0.0;
 }
@@ -189,14 +205,38 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     counter.ensure(1);
     counter.zero(s);
   }
+  if (op.mbox_cap < max_iter + 3) {
+    if (op.mbox_h) FMM_CUDA(cudaFreeHost(op.mbox_h));
+    op.mbox_cap = max_iter + 3;
+    FMM_CUDA(cudaHostAlloc(&op.mbox_h, op.mbox_cap * sizeof(double), cudaHostAllocMapped));
+    FMM_CUDA(cudaHostGetDevicePointer((void**)&op.mbox_d, op.mbox_h, 0));
+  }
+  if (!op.mflag_h) {
+    FMM_CUDA(cudaHostAlloc(&op.mflag_h, sizeof(unsigned long long), cudaHostAllocMapped));
+    FMM_CUDA(cudaHostGetDevicePointer((void**)&op.mflag_d, op.mflag_h, 0));
+    *op.mflag_h = op.mbox_seq;
+  }
+  // wait for the kernel that posts sequence `seq` (spin on pinned memory; a
+  // failed stream surfaces through cudaStreamQuery)
+  auto wait_post = [&](unsigned long long seq) {
+    const volatile unsigned long long* f = op.mflag_h;
+    for (long spins = 0; *f != seq; ++spins) {
+      if ((spins & 1023) == 1023) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e != cudaSuccess && e != cudaErrorNotReady) FMM_CUDA(e);
+        if (e == cudaSuccess && *f != seq) throw CudaFailure("GMRES mailbox: stream idle without a post");
+      }
+    }
+  };
   // ||b||
   double* nb = scal.get() + max_iter + 2;
-  k_norm<<<RB, RT, 0, s>>>(n, const_cast<double*>(b), nullptr, nullptr, partials.get(), counter.get(), nb);
+  const unsigned long long seq_b = ++op.mbox_seq;
+  k_norm<<<RB, RT, 0, s>>>(n, const_cast<double*>(b), nullptr, nullptr, partials.get(), counter.get(), nb,
+                           op.mbox_d, op.mflag_d, seq_b);
   FMM_LAUNCH_CHECK();
   op.kernel_launches += 1;
-  double norm_b = 0.0;
-  FMM_CUDA(cudaMemcpyAsync(&norm_b, nb, sizeof(double), cudaMemcpyDeviceToHost, s));
-  FMM_CUDA(cudaStreamSynchronize(s));
+  wait_post(seq_b);
+  const double norm_b = op.mbox_h[0];
   if (norm_b == 0.0) {
     FMM_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
     FMM_CUDA(cudaStreamSynchronize(s));
@@ -224,14 +264,20 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
       double* pp = partials.get();
       int kk = k;
       int64_t nn = n;
-      void* args[] = {&nn, &kk, &Vc, &w, &pp, &hd};
+      double* mb = op.mbox_d;
+      unsigned long long* mf = op.mflag_d;
+      unsigned long long sq = ++op.mbox_seq;
+      void* args[] = {&nn, &kk, &Vc, &w, &pp, &hd, &mb, &mf, &sq};
       FMM_CUDA(cudaLaunchCooperativeKernel((const void*)k_arnoldi, dim3(AB), dim3(RT), args, 0, s));
     }
     FMM_LAUNCH_CHECK();
     op.kernel_launches += 1;
-    FMM_CUDA(cudaMemcpyAsync(hcol.data(), hd, (k + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
-    FMM_CUDA(cudaStreamSynchronize(s));
-    op_collect_stage_times(op);
+    wait_post(op.mbox_seq);
+    for (int j = 0; j <= k + 1; ++j) hcol[j] = op.mbox_h[j];
+    if (op.timing) {
+      FMM_CUDA(cudaStreamSynchronize(s));
+      op_collect_stage_times(op);
+    }
     for (int j = 0; j <= k + 1; ++j) Hat(j, k) = hcol[j];
     for (int j = 0; j < k; ++j) {
       const double h1 = cs[j] * Hat(j, k) + sn[j] * Hat(j + 1, k);

@@ -303,6 +303,8 @@ void record(BemOp& op, int stage, bool end, cudaStream_t s) {
 
 BemOp::~BemOp() {
   for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  if (mbox_h) cudaFreeHost(mbox_h);
+  if (mflag_h) cudaFreeHost(mflag_h);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : call_ev)

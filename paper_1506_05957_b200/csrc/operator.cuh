@@ -120,6 +120,15 @@ struct BemOp {
   // GMRES workspaces (Krylov basis, reductions), grow-only
   DevBuf<double> g_basis, g_partials, g_scal, g_y;
   DevBuf<unsigned> g_counter;
+  // host-mapped mailbox: the Arnoldi / norm kernels post their scalars and a
+  // sequence number straight into pinned host memory; the host spins on it
+  // instead of a copy + stream synchronisation per iteration
+  double* mbox_h = nullptr;                 // [mbox_cap] values
+  double* mbox_d = nullptr;
+  unsigned long long* mflag_h = nullptr;    // sequence flag
+  unsigned long long* mflag_d = nullptr;
+  int mbox_cap = 0;
+  unsigned long long mbox_seq = 0;
 
   // CUDA graphs of apply(p), one per order
   std::map<int, cudaGraphExec_t> graphs;
