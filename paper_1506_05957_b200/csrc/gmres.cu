@@ -115,10 +115,10 @@ __global__ void k_combine(int64_t n, int m, const double* __restrict__ V, const 
   }
 }
 
-__global__ void k_scale(int64_t n, const double* b, const double* nb, double* v) {
+__global__ void k_scale(int64_t n, const double* b, const double* nb, double* v, double* v2) {
   const double d = *nb;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    v[i] = b[i] / d;
+    v[i] = v2[i] = b[i] / d;
 }
 
 // One Arnoldi step in a single cooperative launch (grid-wide barriers between
@@ -141,9 +141,13 @@ __device__ double grid_total(double part, double* partials, double* sh) {
   return bc;
 }
 
+// (w0: the mat-vec result, read in the first sweep; w: the new basis vector;
+// xnext: a second copy of it, the next mat-vec's input)
 __global__ void __launch_bounds__(RT) k_arnoldi(int64_t n, int k, const double* __restrict__ V,
-                                                double* w, double* partials, double* hd, double* mbox,
-                                                unsigned long long* mflag, unsigned long long seq) {
+                                                const double* __restrict__ w0, double* w,
+                                                double* xnext, double* partials, double* hd,
+                                                double* mbox, unsigned long long* mflag,
+                                                unsigned long long seq) {
   __shared__ double sh[RT / 32];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -153,11 +157,9 @@ __global__ void __launch_bounds__(RT) k_arnoldi(int64_t n, int k, const double* 
     const double* v = j <= k ? V + (size_t)j * n : nullptr;
     double acc = 0.0;
     for (int64_t i = i0; i < n; i += stride) {
-      double wi = w[i];
-      if (vprev) {
-        wi = wi - h * vprev[i];
-        w[i] = wi;
-      }
+      double wi = j ? w[i] : w0[i];
+      if (vprev) wi = wi - h * vprev[i];
+      if (!j || vprev) w[i] = wi;
       acc = v ? fma(v[i], wi, acc) : fma(wi, wi, acc);
     }
     // alternate two partial arrays so a fast block cannot overwrite a slow block's read
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(RT) k_arnoldi(int64_t n, int k, const double* 
     __threadfence_system();
     *reinterpret_cast<volatile unsigned long long*>(mflag) = seq;
   }
-  for (int64_t i = i0; i < n; i += stride) w[i] = h > 0.0 ? w[i] / h : 0.0;
+  for (int64_t i = i0; i < n; i += stride) w[i] = xnext[i] = h > 0.0 ? w[i] / h : 0.0;
 }
 
 double relax_eps(double r, double eta) { return std::min(eta / std::min(std::max(r, eta), 1.0), 1.0); }
@@ -245,7 +247,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   }
   DevBuf<double>& V = op.g_basis;
   V.ensure((size_t)(max_iter + 1) * n);
-  k_scale<<<RB, RT, 0, s>>>(n, b, nb, V.get());
+  k_scale<<<RB, RT, 0, s>>>(n, b, nb, V.get(), op.x_in.get());
   op.kernel_launches += 1;
   std::vector<double> H((size_t)(max_iter + 1) * std::max(max_iter, 1), 0.0);
   auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * max_iter + j]; };
@@ -258,7 +260,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     int p = relaxed ? std::min(schedule_p(residual, tol, p_initial, p_min), prev_p) : p_initial;
     prev_p = p;
     double* w = V.get() + (size_t)(k + 1) * n;
-    op_apply_device(op, V.get() + (size_t)k * n, w, p);
+    op_apply_device(op, nullptr, nullptr, p);  // x_in holds v_k (k_scale / k_arnoldi)
     {
       const double* Vc = V.get();
       double* pp = partials.get();
@@ -267,7 +269,9 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
       double* mb = op.mbox_d;
       unsigned long long* mf = op.mflag_d;
       unsigned long long sq = ++op.mbox_seq;
-      void* args[] = {&nn, &kk, &Vc, &w, &pp, &hd, &mb, &mf, &sq};
+      const double* w0 = op.y_out.get();
+      double* xn = op.x_in.get();
+      void* args[] = {&nn, &kk, &Vc, &w0, &w, &xn, &pp, &hd, &mb, &mf, &sq};
       FMM_CUDA(cudaLaunchCooperativeKernel((const void*)k_arnoldi, dim3(AB), dim3(RT), args, 0, s));
     }
     FMM_LAUNCH_CHECK();

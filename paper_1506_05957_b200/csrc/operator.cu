@@ -511,7 +511,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
   sys_call(op, p, false, op.x_in.get(), op.y_out.get(), c);
   prepare(op, c.kind, p, false);
   cudaStream_t s = op.s_main;
-  FMM_CUDA(cudaMemcpyAsync(op.x_in.get(), x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (x) FMM_CUDA(cudaMemcpyAsync(op.x_in.get(), x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   const bool sharded = op.shard.active;
   if (op.use_graphs && !(sharded && !op.shard.virtual_mode)) {
     // captured graphs bake in buffer addresses: any reallocation invalidates them
@@ -559,7 +559,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
   } else {
     op_layer(op, c, s, sharded);
   }
-  FMM_CUDA(cudaMemcpyAsync(y, op.y_out.get(), op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (y) FMM_CUDA(cudaMemcpyAsync(y, op.y_out.get(), op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
 // stage timers of the last apply; call only after the op's stream has been synchronised

@@ -167,7 +167,9 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t n_panels, const do
              int n_gauss_singular, int formulation, double theta, int n_crit, double mu,
              double near_factor, int max_depth);
 void op_layer(BemOp& op, const LayerCall& call, cudaStream_t s, bool sharded = false);
-void op_apply_device(BemOp& op, const double* x, double* y, int p);  // async on op.s_main
+// async on op.s_main; x == nullptr: the input is already in op.x_in, y == nullptr:
+// leave the result in op.y_out
+void op_apply_device(BemOp& op, const double* x, double* y, int p);
 void op_collect_stage_times(BemOp& op);  // after a sync of op.s_main
 void op_dense_apply_device(BemOp& op, const double* x, double* y);
 void op_rhs_device(BemOp& op, const double* data, double* b, int p, bool dense);
