@@ -61,9 +61,31 @@ inline int p2p_comps(P2PKind k) { return (k == P2PKind::LAP_Q || k == P2PKind::L
 // Source strengths (sorted source order): LAP_Q: w[ns]; LAP_D: w[ns*3] dipoles;
 // STOKESLET: w[ns*3] forces; STRESSLET: w[ns*6] = (force, normal).
 // CTA b takes item order[b] (largest work first), or item b when order is null.
+// Per item list, for the persistent double-layer kernel: every item's source leaves as
+// (start, count, tile offset) at their CSR position, and every item target's tile slot of
+// its own centroid Gauss point (-1 if not in the item) at its partial-sum position.
+struct LapdHdr {  // one P2P item in schedule (largest-first) order
+  int item, pair_begin, nl, ns, t0, nt, out_off, pad;
+  double cx, cy, cz, pad2;  // target leaf centre
+};
+struct P2PAux {
+  DevBuf<LapdHdr> hdr;
+  int n_items = 0;
+  DevBuf<int4> ltab;
+  DevBuf<int> slot;
+  int max_leaves = 1, max_tgt = 1;
+  bool ready = false;
+  void build(const Tree& S, const Tree& T, const std::vector<P2PItem>& items,
+             const std::vector<int>& p2p_src, const std::vector<int>& self_src_sorted, cudaStream_t st);
+};
+// aux (LAP_D) selects the persistent expanded-form double-layer kernel, which also needs a
+// 2-uint schedule counter (zero before the first launch; self-resetting) and the sources as
+// records srec[3 i .. 3 i + 2] = (x, y), (z, d_x), (d_y, d_z) in sorted order; without them, or
+// when the stages do not fit shared memory, the difference-form kernel runs.
 void launch_p2p(P2PKind kind, const TreeDev& S, const TreeDev& T, const P2PItem* items,
                 int n_items, const int* p2p_src, int max_sources, const double* w, double* part,
-                cudaStream_t st, const int* order);
+                cudaStream_t st, const int* order, const P2PAux* aux = nullptr,
+                unsigned* sched = nullptr, const double2* srec = nullptr);
 
 // generic channel near field (FmmPlan.near_field): charges q[C][ns] and/or dipoles d[C][ns][3];
 // accumulates into pot[C][nt] (+ grad[C][nt][3]) in ORIGINAL target order.

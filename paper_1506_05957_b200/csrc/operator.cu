@@ -23,12 +23,19 @@ namespace {
 constexpr double FOUR_PI = 12.566370614359172;
 
 __global__ void k_sorted_sources(int64_t ns, const int* perm, const double* gw, double* s_w,
-                                 int* s_panel) {
+                                 int* s_panel, const int* tgt_perm_inv, int* self_src) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= ns) return;
   const int o = perm[i];
   s_w[i] = gw[o];
   s_panel[i] = o / 4;  // 4 far-rule points per panel, panel-major (bemop.py:68-70)
+  // Gauss point 0 of panel j is bitwise its collocation point (bemop.py:64-67)
+  if (o % 4 == 0) self_src[tgt_perm_inv[o / 4]] = (int)i;
+}
+
+__global__ void k_invert_perm(int64_t n, const int* perm, int* inv) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) inv[perm[i]] = (int)i;
 }
 
 // Gauss-point densities w_g * x[panel(g)] in sorted source order (bemop.py:188-190)
@@ -36,7 +43,8 @@ template <int KIND>
 __global__ void k_density(int64_t ns, const double* __restrict__ s_w, const int* __restrict__ s_panel,
                           const double* __restrict__ px, const double* __restrict__ py,
                           const double* __restrict__ pz, const double* __restrict__ nrm,
-                          const double* __restrict__ x, double* q, double* dip, double* wsrc) {
+                          const double* __restrict__ x, double* q, double* dip, double* wsrc,
+                          double2* __restrict__ srec) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= ns) return;
   const int pn = s_panel[i];
@@ -45,9 +53,14 @@ __global__ void k_density(int64_t ns, const double* __restrict__ s_w, const int*
     q[i] = w * x[pn];
   } else if (KIND == K_LAP_DOUBLE) {
     const double v = w * x[pn];
-    dip[3 * i] = v * nrm[3 * pn];
-    dip[3 * i + 1] = v * nrm[3 * pn + 1];
-    dip[3 * i + 2] = v * nrm[3 * pn + 2];
+    const double d0 = v * nrm[3 * pn], d1 = v * nrm[3 * pn + 1], d2 = v * nrm[3 * pn + 2];
+    dip[3 * i] = d0;
+    dip[3 * i + 1] = d1;
+    dip[3 * i + 2] = d2;
+    // the near field's source records (x, y), (z, d_x), (d_y, d_z)
+    srec[3 * i] = make_double2(px[i], py[i]);
+    srec[3 * i + 1] = make_double2(pz[i], d0);
+    srec[3 * i + 2] = make_double2(d1, d2);
   } else {
     const double f0 = w * x[3 * pn], f1 = w * x[3 * pn + 1], f2 = w * x[3 * pn + 2];
     const double yf = px[i] * f0 + py[i] * f1 + pz[i] * f2;
@@ -221,7 +234,7 @@ void launch_density(BemOp& op, const double* x, cudaStream_t s) {
   const int64_t ns = op.plan.src.n_points;
   k_density<KIND><<<grid_for(ns, 256), 256, 0, s>>>(
       ns, op.s_weight.get(), op.s_panel.get(), op.plan.src.px.get(), op.plan.src.py.get(),
-      op.plan.src.pz.get(), op.normal.get(), x, op.q.get(), op.dip.get(), op.wsrc.get());
+      op.plan.src.pz.get(), op.normal.get(), x, op.q.get(), op.dip.get(), op.wsrc.get(), op.srec.get());
   FMM_LAUNCH_CHECK();
 }
 
@@ -278,6 +291,7 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
   op.q.ensure((size_t)ns * (kind == K_STOKESLET ? 4 : 1));
   op.dip.ensure((size_t)ns * 3 * (kind == K_STRESSLET ? 7 : 1));
   op.wsrc.ensure((size_t)ns * 6);
+  op.srec.ensure((size_t)ns * 3);
   if (dense) {
     ensure_dense(op);
     op.part_dense.ensure((size_t)std::max<int64_t>(op.dense_part_len, 1) * 3);
@@ -334,8 +348,9 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   // the near field (one large, independent launch) fills the remaining SMs
   int prio_lo = 0, prio_hi = 0;
   FMM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  FMM_CUDA(cudaStreamCreateWithPriority(&op.s_main, cudaStreamNonBlocking, prio_hi));
-  FMM_CUDA(cudaStreamCreateWithPriority(&op.s_near, cudaStreamNonBlocking, prio_lo));
+  const bool near_hi = std::getenv("FMMBEM_NEAR_PRIO_HIGH") != nullptr;
+  FMM_CUDA(cudaStreamCreateWithPriority(&op.s_main, cudaStreamNonBlocking, near_hi ? prio_lo : prio_hi));
+  FMM_CUDA(cudaStreamCreateWithPriority(&op.s_near, cudaStreamNonBlocking, near_hi ? prio_hi : prio_lo));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_join, cudaEventDisableTiming));
   for (auto& e : op.ev) FMM_CUDA(cudaEventCreate(&e));
@@ -359,9 +374,22 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   const int64_t ns = op.plan.src.n_points;
   op.s_weight.resize(ns);
   op.s_panel.resize(ns);
-  k_sorted_sources<<<grid_for(ns, 256), 256, 0, s>>>(ns, op.plan.src.perm.get(), op.gauss_w.get(),
-                                                      op.s_weight.get(), op.s_panel.get());
-  FMM_LAUNCH_CHECK();
+  op.self_src.resize(P);
+  op.p2p_sched.resize(2);
+  op.p2p_sched.zero(s);
+  {
+    DevBuf<int> tinv;
+    tinv.resize(P);
+    k_invert_perm<<<grid_for(P, 256), 256, 0, s>>>(P, op.plan.tgt.perm.get(), tinv.get());
+    FMM_LAUNCH_CHECK();
+    k_sorted_sources<<<grid_for(ns, 256), 256, 0, s>>>(ns, op.plan.src.perm.get(), op.gauss_w.get(),
+                                                        op.s_weight.get(), op.s_panel.get(), tinv.get(),
+                                                        op.self_src.get());
+    FMM_LAUNCH_CHECK();
+    FMM_CUDA(cudaStreamSynchronize(s));
+    op.h_self_src = op.self_src.download(s);
+  }
+  op.p2p_aux.build(op.plan.src, op.plan.tgt, op.plan.items, op.plan.h_p2p_src, op.h_self_src, s);
   op.max_item_sources = 0;
   for (const auto& it : op.plan.items) {
     int acc = 0;
@@ -408,10 +436,12 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
                nullptr);
   else if (sharded)
     launch_p2p((P2PKind)c.kind, S, T, sw.items.get(), (int)sw.items_h.size(), pl.p2p_src.get(),
-               sw.max_item_sources, w, op.part.get(), op.s_near, sw.p2p_order.get());
+               sw.max_item_sources, w, op.part.get(), op.s_near, sw.p2p_order.get(), &sw.p2p_aux,
+               op.p2p_sched.get(), op.srec.get());
   else
     launch_p2p((P2PKind)c.kind, S, T, pl.d_items.get(), (int)pl.items.size(), pl.p2p_src.get(),
-               op.max_item_sources, w, op.part.get(), op.s_near, pl.p2p_order.get());
+               op.max_item_sources, w, op.part.get(), op.s_near, pl.p2p_order.get(), &op.p2p_aux,
+               op.p2p_sched.get(), op.srec.get());
   record(op, ST_P2P, true, op.s_near);
   FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
   // far field on the main stream
@@ -515,7 +545,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
   const bool sharded = op.shard.active;
   if (op.use_graphs && !(sharded && !op.shard.virtual_mode)) {
     // captured graphs bake in buffer addresses: any reallocation invalidates them
-    const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.part.get(),
+    const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.srec.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
                                           op.x_in.get(), op.y_out.get(), op.m2l_part.get(),
                                           op.p2m_basis.get(), op.m2m_cout.get(), op.plan.rotf.get(),

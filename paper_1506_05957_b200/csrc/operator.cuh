@@ -34,6 +34,7 @@ struct ShardWork {
   std::vector<P2PItem> items_h;
   DevBuf<P2PItem> items;
   DevBuf<int> p2p_order;
+  P2PAux p2p_aux;
   DevBuf<int> item_begin;
   int64_t part_len = 0;
   int max_item_sources = 0;
@@ -78,6 +79,10 @@ struct BemOp {
   // per sorted source: weight, panel, absolute position is plan.src.p{x,y,z}
   DevBuf<double> s_weight;
   DevBuf<int> s_panel;
+  DevBuf<int> self_src;  // per sorted target: sorted source index of its centroid Gauss point
+  DevBuf<unsigned> p2p_sched;  // persistent P2P item counter + CTAs done (self-resetting)
+  std::vector<int> h_self_src;
+  P2PAux p2p_aux;  // plan items
 
   // near pairs (CSR by target panel) and the two corrections
   int near_nnz = 0;
@@ -85,6 +90,7 @@ struct BemOp {
   Correction c_sys, c_rhs;
 
   // work buffers
+  DevBuf<double2> srec;  // double-layer near-field source records (k_density)
   DevBuf<double> x_in, y_out, q, dip, wsrc, part, part_dense, stage_x, stage_y;
   DevBuf<double2> M, L, m2l_part, m2m_cout;
   int max_item_sources = 0;

@@ -181,6 +181,318 @@ k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __rest
   }
 }
 
+// ------------------------------------------------------------------ double layer, expanded form
+// Laplace double-layer potential sum_j d_j.(t - y_j) / |t - y_j|^3 (fmm.py:399-419) in
+// coordinates centred on the target leaf (t' = t - c, s' = y - c):
+//   |t - y|^2 = |t'|^2 + |s'|^2 - 2 t'.s'      (1 DADD + 3 DFMA instead of 3 DADD + 3 DFMA)
+//   d.(t - y) = d.t' - d.s'                    (3 DFMA)
+// with the per-source parts (-2 s', |s'|^2, d, -d.s') staged once per item.  Centring on the
+// leaf keeps |t'|, |s'| at the size of the near region, so the cancellation in |t - y|^2 costs
+// ~eps R^2 / r^2 <= ~1e-12 relative on the closest pairs.  The coincident pair (the target is
+// Gauss point 0 of its own panel, bemop.py:64-67; the reference's d2 > 0 mask, fmm.py:403) is
+// removed by index: its slot in the staged tile gets d2 = ~1e300, so r^-3 underflows to 0.
+// 13 DP instructions per interaction (15 in the difference form).
+//
+// Persistent and warp-specialised: one CTA per SM; LAPD_PROD producer warps take items in
+// largest-first order from a global counter and stage item k+1 (leaf table, transformed
+// sources, every target's own-source slot) into one of two shared-memory stages while the
+// LAPD_CONS consumer threads run the interaction loop on item k.  Stages are handed over
+// with named barriers (FULL: producers arrive, consumers wait; EMPTY: the reverse).
+constexpr int LAPD_TPT = 4;
+constexpr int LAPD_CONS = 256;
+constexpr int LAPD_PROD = 128;
+enum : int { BAR_FULL0 = 1, BAR_EMPTY0 = 5, BAR_PROD = 9 };  // up to 4 stages
+
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct LapdStage {  // shared-memory stage layout (offsets in bytes from the stage base)
+  size_t planes, tgt, ltab, slot, bytes;
+  __host__ __device__ LapdStage(int max_src, int max_leaves, int max_tgt) {
+    planes = 0;
+    tgt = (size_t)4 * max_src * sizeof(double2);        // [2][max_tgt] double2: (x', y'), (z', |t'|^2)
+    ltab = tgt + (size_t)2 * max_tgt * sizeof(double2);
+    slot = ltab + (size_t)max_leaves * sizeof(int4);
+    bytes = (slot + (size_t)max_tgt * sizeof(int) + 4 * sizeof(int) + 15) / 16 * 16;
+  }
+};
+
+template <int NCT, int NSTG>
+__global__ void __launch_bounds__(NCT + LAPD_PROD, 1)
+k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4* __restrict__ gl_ltab,
+           const int* __restrict__ gl_slot, int max_src, int max_leaves, int max_tgt,
+           const double2* __restrict__ srec, double* __restrict__ part, unsigned* __restrict__ sched,
+           long long* __restrict__ trace) {
+  constexpr int TPT = LAPD_TPT, NPT = LAPD_PROD, ALL = NCT + NPT;
+  // optional per-item clock trace (FMMBEM_P2P_TRACE): [cta][item < 32][8]
+#define TR(k, j)                                                              \
+  if (trace && (k) < 32) trace[((size_t)blockIdx.x * 32 + (k)) * 8 + (j)] = clock64()
+  extern __shared__ __align__(16) unsigned char smem[];
+  const LapdStage L(max_src, max_leaves, max_tgt);
+  double* red = reinterpret_cast<double*>(smem + NSTG * L.bytes);  // [NSTG][NCT * TPT] group partials
+  __shared__ int s_idx;
+  __shared__ unsigned s_done[NSTG];  // consumer warps done with the stage's item
+  if (threadIdx.x < NSTG) s_done[threadIdx.x] = 0u;
+  __syncthreads();
+  if (threadIdx.x >= NCT) {
+    // ------------------------------------------------------------------ producers
+    // schedule position blockIdx.x first, then positions gridDim.x + atomicAdd(sched) (the next
+    // one requested while the current item is staged)
+    const int pt = threadIdx.x - NCT;
+    int k = 0, cur = blockIdx.x;
+    unsigned nxt = 0;
+    for (;; ++k) {
+      const int st = k % NSTG;
+      unsigned char* base = smem + st * L.bytes;
+      double2* sh2 = reinterpret_cast<double2*>(base);
+      int4* ltab = reinterpret_cast<int4*>(base + L.ltab);
+      int* slot = reinterpret_cast<int*>(base + L.slot);
+      double2* tg = reinterpret_cast<double2*>(base + L.tgt);
+      int* hdr = slot + max_tgt;  // live (0: done), ns, nt, out_off
+      if (pt == 0) TR(k, 0);
+      if (k >= NSTG) bar_sync(BAR_EMPTY0 + st, ALL);
+      if (pt == 0) TR(k, 1);
+      if (k > 0) {
+        if (pt == 0) s_idx = (int)(gridDim.x + nxt);
+        bar_sync(BAR_PROD, NPT);
+        cur = s_idx;
+      }
+      if (pt == 0) nxt = atomicAdd(sched, 1u);
+      if (cur >= n_items) {
+        if (pt == 0) hdr[0] = 0;
+        bar_arrive(BAR_FULL0 + st, ALL);
+        break;
+      }
+      const LapdHdr H = hdrs[cur];
+      for (int q = pt; q < H.nl; q += NPT) ltab[q] = gl_ltab[H.pair_begin + q];
+      for (int lt = pt; lt < H.nt; lt += NPT) {
+        slot[lt] = gl_slot[H.out_off + lt];
+        const double x = T.px[H.t0 + lt] - H.cx, y = T.py[H.t0 + lt] - H.cy, z = T.pz[H.t0 + lt] - H.cz;
+        tg[lt] = make_double2(x, y);
+        tg[max_tgt + lt] = make_double2(z, fma(x, x, fma(y, y, z * z)));
+      }
+      if (pt == 0) {
+        hdr[0] = 1;
+        hdr[1] = H.ns;
+        hdr[2] = H.nt;
+        hdr[3] = H.out_off;
+      }
+      bar_sync(BAR_PROD, NPT);
+      // flattened over the tile: 4 sources per thread per round, loads issued before use
+      for (int i0 = pt; i0 < H.ns; i0 += 4 * NPT) {
+        double2 v[4][3];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = min(i0 + u * NPT, H.ns - 1);
+          int lo = 0, hi = H.nl - 1;  // last leaf with offset <= i
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (ltab[mid].z <= i) lo = mid;
+            else hi = mid - 1;
+          }
+          const int4 e = ltab[lo];
+          const size_t g = (size_t)(e.x + i - e.z) * 3;
+          v[u][0] = srec[g];
+          v[u][1] = srec[g + 1];
+          v[u][2] = srec[g + 2];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * NPT;
+          if (i >= H.ns) break;
+          const double sx = v[u][0].x - H.cx, sy = v[u][0].y - H.cy, sz = v[u][1].x - H.cz;
+          const double dx = v[u][1].y, dy = v[u][2].x, dz = v[u][2].y;
+          const double ss = fma(sx, sx, fma(sy, sy, sz * sz));
+          const double ds = fma(dx, sx, fma(dy, sy, dz * sz));
+          sh2[i] = make_double2(-2.0 * sx, -2.0 * sy);
+          sh2[max_src + i] = make_double2(-2.0 * sz, ss);
+          sh2[2 * max_src + i] = make_double2(dx, dy);
+          sh2[3 * max_src + i] = make_double2(dz, -ds);
+        }
+      }
+      if (pt == 0) TR(k, 2);
+      bar_arrive(BAR_FULL0 + st, ALL);
+    }
+    // match the consumers' EMPTY arrivals of the last NSTG - 1 items
+    for (int j = max(0, k - NSTG + 1); j < k; ++j) bar_sync(BAR_EMPTY0 + j % NSTG, ALL);
+    __syncwarp();
+    if (threadIdx.x == NCT) {
+      // the last CTA out resets the schedule for the next launch
+      __threadfence();
+      if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+        sched[0] = 0u;
+        sched[1] = 0u;
+        __threadfence();
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------------- consumers
+  for (int k = 0;; ++k) {
+    const int st = k % NSTG;
+    const unsigned char* base = smem + st * L.bytes;
+    const double2* sh2 = reinterpret_cast<const double2*>(base);
+    const int* slot = reinterpret_cast<const int*>(base + L.slot);
+    const double2* tg = reinterpret_cast<const double2*>(base + L.tgt);
+    const int* hdr = slot + max_tgt;
+    if (threadIdx.x == 0) TR(k, 3);
+    bar_sync(BAR_FULL0 + st, ALL);
+    if (threadIdx.x == 0) TR(k, 4);
+    if (hdr[0] == 0) break;
+    const int ns = hdr[1], nt = hdr[2], out_off = hdr[3];
+    // thread groups: nsl target slots (TPT targets each) x G source groups
+    const int nsl = (nt + TPT - 1) / TPT;
+    const int G = NCT / nsl;
+    const int sl = threadIdx.x % nsl, g = threadIdx.x / nsl;
+    double acc[TPT], tx[TPT], ty[TPT], tz[TPT], tt[TPT];
+    int self[TPT];
+#pragma unroll
+    for (int q = 0; q < TPT; ++q) {
+      const int lt = min(sl + q * nsl, nt - 1);
+      const double2 xy = tg[lt], zt = tg[max_tgt + lt];
+      tx[q] = xy.x;
+      ty[q] = xy.y;
+      tz[q] = zt.x;
+      tt[q] = zt.y;
+      acc[q] = 0.0;
+      self[q] = slot[lt];
+    }
+    if (g < G) {
+      for (int j = g; j < ns; j += G) {
+        const double2 ab = sh2[j], cs = sh2[max_src + j], dxy = sh2[2 * max_src + j],
+                      dzs = sh2[3 * max_src + j];
+#pragma unroll
+        for (int q = 0; q < TPT; ++q) {
+          double d2 = fma(tx[q], ab.x, fma(ty[q], ab.y, fma(tz[q], cs.x, cs.y + tt[q])));
+          // coincident pair: hi word of ~1e300 (the lo word is irrelevant)
+          d2 = __hiloint2double(j == self[q] ? 0x7E37E43C : __double2hiint(d2), __double2loint(d2));
+          double y;
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
+          const double y2 = y * y;
+          const double y3 = y2 * y;
+          const double e = fma(-d2, y2, 1.0);
+          const double rn = fma(dxy.x, tx[q], fma(dxy.y, ty[q], fma(dzs.x, tz[q], dzs.y)));
+          acc[q] = fma(rn, fma(1.5 * e, y3, y3), acc[q]);
+        }
+      }
+    }
+    if (threadIdx.x == 0) TR(k, 5);
+    if (threadIdx.x == NCT - 32) TR(k, 6);
+    // group partials into this stage's reduction area; the last warp to finish sums them in
+    // group order (deterministic) while the others move on to the next stage
+    double* rd = red + st * NCT * TPT;
+    if (g < G)
+#pragma unroll
+      for (int q = 0; q < TPT; ++q) rd[(g * TPT + q) * nsl + sl] = acc[q];
+    __threadfence_block();
+    __syncwarp();
+    unsigned last = 0;
+    if ((threadIdx.x & 31) == 0) last = atomicAdd(&s_done[st], 1u) == NCT / 32 - 1;
+    if (__shfl_sync(0xffffffffu, last, 0)) {
+      __threadfence_block();
+      for (int lt = threadIdx.x & 31; lt < nt; lt += 32) {
+        const int q = lt / nsl, s2 = lt - q * nsl;
+        double r = 0.0;
+        for (int gg = 0; gg < G; ++gg) r += rd[(gg * TPT + q) * nsl + s2];
+        part[out_off + lt] = r;
+      }
+      if ((threadIdx.x & 31) == 0) s_done[st] = 0u;
+      __syncwarp();
+    }
+    bar_arrive(BAR_EMPTY0 + st, ALL);  // stage (and, for the last warp, its reduction area) released
+    if (threadIdx.x == 0) TR(k, 7);
+  }
+}
+
+long long* p2p_trace_buffer();
+
+void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& items,
+                   const std::vector<int>& p2p_src, const std::vector<int>& self_src_sorted,
+                   cudaStream_t st) {
+  std::vector<int4> lt(std::max<size_t>(p2p_src.size(), 1), make_int4(0, 0, 0, 0));
+  int64_t part_len = 0;
+  for (const auto& it : items) part_len = std::max<int64_t>(part_len, it.out_off + T.h_body_count[it.tgt_leaf]);
+  std::vector<int> sl(std::max<int64_t>(part_len, 1), -1);
+  max_leaves = 1;
+  max_tgt = 1;
+  for (const auto& it : items) {
+    int off = 0;
+    for (int k = it.pair_begin; k < it.pair_end; ++k) {
+      const int leaf = p2p_src[k];
+      lt[k] = make_int4(S.h_body_start[leaf], S.h_body_count[leaf], off, 0);
+      off += S.h_body_count[leaf];
+    }
+    const int t0 = T.h_body_start[it.tgt_leaf], nt = T.h_body_count[it.tgt_leaf];
+    for (int l = 0; l < nt; ++l) {
+      const int gs = self_src_sorted[t0 + l];
+      for (int k = it.pair_begin; k < it.pair_end; ++k)
+        if (gs >= lt[k].x && gs < lt[k].x + lt[k].y) sl[it.out_off + l] = lt[k].z + gs - lt[k].x;
+    }
+    max_leaves = std::max(max_leaves, it.pair_end - it.pair_begin);
+    max_tgt = std::max(max_tgt, nt);
+  }
+  const std::vector<int> ord = p2p_schedule(T, S, items, p2p_src);
+  std::vector<LapdHdr> h(std::max<size_t>(ord.size(), 1));
+  for (size_t r = 0; r < ord.size(); ++r) {
+    const P2PItem& it = items[ord[r]];
+    LapdHdr& e = h[r];
+    e.item = ord[r];
+    e.pair_begin = it.pair_begin;
+    e.nl = it.pair_end - it.pair_begin;
+    e.ns = it.pair_end > it.pair_begin ? lt[it.pair_end - 1].z + lt[it.pair_end - 1].y : 0;
+    e.t0 = T.h_body_start[it.tgt_leaf];
+    e.nt = T.h_body_count[it.tgt_leaf];
+    e.out_off = it.out_off;
+    e.cx = T.h_cx[it.tgt_leaf];
+    e.cy = T.h_cy[it.tgt_leaf];
+    e.cz = T.h_cz[it.tgt_leaf];
+  }
+  n_items = (int)items.size();
+  p2p_trace_buffer();  // (allocated here, outside any stream capture)
+  hdr.upload(h, st);
+  ltab.upload(lt, st);
+  slot.upload(sl, st);
+  ready = true;
+}
+
+// FMMBEM_P2P_TRACE=1: a per-item clock trace of the double-layer kernel, read by fmmbem_debug_p2p_trace
+long long* p2p_trace_buffer() {
+  static long long* buf = nullptr;
+  if (!buf && std::getenv("FMMBEM_P2P_TRACE")) {
+    FMM_CUDA(cudaMalloc(&buf, (size_t)1024 * 32 * 8 * sizeof(long long)));
+    FMM_CUDA(cudaMemset(buf, 0, (size_t)1024 * 32 * 8 * sizeof(long long)));
+  }
+  return buf;
+}
+
+void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const double2* srec, double* part,
+                     cudaStream_t st, unsigned* sched) {
+  const LapdStage L(max_src, aux.max_leaves, aux.max_tgt);
+  static const int nct = std::getenv("FMMBEM_P2P_NCT") ? std::atoi(std::getenv("FMMBEM_P2P_NCT")) : LAPD_CONS;
+  const size_t per = L.bytes + (size_t)nct * LAPD_TPT * sizeof(double);
+  static const int want = std::getenv("FMMBEM_P2P_STAGES") ? std::atoi(std::getenv("FMMBEM_P2P_STAGES")) : 3;
+  const int nstg = (want >= 3 && 3 * per <= 227 * 1024) ? 3 : 2;
+  const size_t smem = nstg * per;
+  FMM_REQUIRE(smem <= 227 * 1024, "P2P: source slice too large for shared memory");
+  FMM_REQUIRE(sched != nullptr, "P2P: the double-layer kernel needs its schedule counter");
+  auto kern = nstg == 3 ? (nct == 384 ? k_p2p_lapd<384, 3> : k_p2p_lapd<LAPD_CONS, 3>)
+                        : (nct == 384 ? k_p2p_lapd<384, 2> : k_p2p_lapd<LAPD_CONS, 2>);
+  const int nthr = (nct == 384 ? nct : LAPD_CONS) + LAPD_PROD;
+  FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 0;
+  FMM_CUDA(cudaGetDevice(&dev));
+  FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::min(aux.n_items, sms);
+  if (grid > 0)
+    kern<<<grid, nthr, smem, st>>>(T, aux.hdr.get(), aux.n_items, aux.ltab.get(), aux.slot.get(), max_src,
+                                   aux.max_leaves, aux.max_tgt, srec, part, sched, p2p_trace_buffer());
+  FMM_LAUNCH_CHECK();
+}
+
 template <P2PKind K>
 void launch_p2p_t(const TreeDev& S, const TreeDev& T, const P2PItem* items, int n_items,
                   const int* p2p_src, int max_src, const double* w, double* part, cudaStream_t st,
@@ -198,11 +510,18 @@ void launch_p2p_t(const TreeDev& S, const TreeDev& T, const P2PItem* items, int 
 
 void launch_p2p(P2PKind kind, const TreeDev& S, const TreeDev& T, const P2PItem* items,
                 int n_items, const int* p2p_src, int max_sources, const double* w, double* part,
-                cudaStream_t st, const int* order) {
+                cudaStream_t st, const int* order, const P2PAux* aux, unsigned* sched,
+                const double2* srec) {
   const int ms = std::max(max_sources, 1);
   switch (kind) {
     case P2PKind::LAP_Q: return launch_p2p_t<P2PKind::LAP_Q>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
-    case P2PKind::LAP_D: return launch_p2p_t<P2PKind::LAP_D>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
+    case P2PKind::LAP_D:
+      if (aux && aux->ready && sched && srec &&
+          aux->max_tgt <= LAPD_CONS * LAPD_TPT &&
+          2 * (LapdStage(ms, aux->max_leaves, aux->max_tgt).bytes +
+               (size_t)384 * LAPD_TPT * sizeof(double)) <= 227 * 1024)
+        return launch_p2p_lapd(T, *aux, ms, srec, part, st, sched);
+      return launch_p2p_t<P2PKind::LAP_D>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
     case P2PKind::STOKESLET: return launch_p2p_t<P2PKind::STOKESLET>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
     case P2PKind::STRESSLET: return launch_p2p_t<P2PKind::STRESSLET>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
   }
@@ -351,3 +670,11 @@ void launch_l2p_channels(const TreeDev& T, const int* leaves, int n_leaves, int 
 }
 
 }  // namespace fmmbem
+
+extern "C" int fmmbem_debug_p2p_trace(long long* host, int64_t n) {
+  long long* b = fmmbem::p2p_trace_buffer();
+  if (!b) return 1;
+  if (cudaDeviceSynchronize() != cudaSuccess) return 2;
+  const size_t m = std::min<size_t>((size_t)n, (size_t)1024 * 32 * 8);
+  return cudaMemcpy(host, b, m * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 3;
+}

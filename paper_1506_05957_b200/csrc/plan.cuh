@@ -39,7 +39,7 @@ struct Tree {
   const double* rec = nullptr;  // plan's reciprocal table (common.cuh)
 };
 
-constexpr int P2P_ITEM_SOURCES = 1024;  // sources per P2P work item (shared-memory tile)
+constexpr int P2P_ITEM_SOURCES = 896;   // sources per P2P work item (shared-memory tile)
 
 struct P2PItem {
   int tgt_leaf;   // target cell id

@@ -198,6 +198,7 @@ void op_shard_setup(BemOp& op, int rank, int world, const int* tb, const int* sb
     sw.p2p_order.upload(ord.empty() ? std::vector<int>(1, 0) : ord, s);
   }
   sw.item_begin.upload(ib, s);
+  sw.p2p_aux.build(op.plan.src, op.plan.tgt, sw.items_h, op.plan.h_p2p_src, op.h_self_src, s);
   op.part.ensure((size_t)std::max<int64_t>(std::max(sw.part_len, pl.part_len), 1) * 3);
   // needed target cells: ancestors-or-self of own leaves
   std::vector<uint8_t> need(T.n_cells, 0);

@@ -1,0 +1,50 @@
+"""Per-item clock trace of the persistent double-layer P2P kernel (FMMBEM_P2P_TRACE=1).
+
+python tools/p2p_trace.py cfg2 12
+Per CTA and item: producer (wait EMPTY, stage) and consumer (wait FULL, loop warp 0 / last warp,
+reduce) phases in cycles; summarised over CTAs.
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+os.environ["FMMBEM_P2P_TRACE"] = "1"
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+from paper_1506_05957_b200 import _native  # noqa: E402
+from paper_1506_05957_b200.configs import CONFIGS  # noqa: E402
+from paper_1506_05957_b200.operator import GpuBemOperator  # noqa: E402
+
+name, p = sys.argv[1], int(sys.argv[2])
+cfg = CONFIGS[name]
+op = GpuBemOperator(cfg.mesh(), cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu)
+x = np.random.default_rng(1).uniform(-1, 1, op.shape[0])
+for _ in range(3):
+    op.apply(x, p)
+lib = _native.load()
+buf = np.zeros(1024 * 32 * 8, dtype=np.int64)
+lib.fmmbem_debug_p2p_trace.restype = ctypes.c_int
+lib.fmmbem_debug_p2p_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(buf.size))
+t = buf.reshape(1024, 32, 8)
+ctas = [c for c in range(1024) if t[c, 0, 3] != 0]
+tot = {k: 0 for k in ("p_wait", "p_stage", "c_wait", "c_loop0", "c_looplast", "c_red", "span")}
+for c in ctas:
+    items = [k for k in range(32) if t[c, k, 4] != 0]
+    start = t[c, 0, 3]
+    end = max(t[c, k, 7] for k in items if t[c, k, 7] != 0) if items else start
+    tot["span"] += end - start
+    for k in items:
+        if t[c, k, 0]:
+            tot["p_wait"] += t[c, k, 1] - t[c, k, 0]
+            if t[c, k, 2]:
+                tot["p_stage"] += t[c, k, 2] - t[c, k, 1]
+        tot["c_wait"] += t[c, k, 4] - t[c, k, 3]
+        if t[c, k, 5]:
+            tot["c_loop0"] += t[c, k, 5] - t[c, k, 4]
+            tot["c_looplast"] += t[c, k, 6] - t[c, k, 4]
+            tot["c_red"] += t[c, k, 7] - t[c, k, 5]
+n = max(len(ctas), 1)
+print(name, p, "ctas", len(ctas), {k: round(v / n) for k, v in tot.items()})
+for c in ctas[:2]:
+    print("cta", c, [list(map(int, t[c, k] - t[c, 0, 3])) for k in range(8) if t[c, k, 3]])
