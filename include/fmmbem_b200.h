@@ -124,6 +124,9 @@ int fmmbem_op_gmres_device(fmmbem_op* op, const double* b_dev, double tol, int p
  * and the number of timed applies, reset them; use_graphs toggles CUDA graphs. */
 int fmmbem_op_set_timing(fmmbem_op* op, int enable, int use_graphs);
 int fmmbem_op_stage_times(fmmbem_op* op, double* ms6, int64_t* calls, int reset);
+/* serial = 1 runs the near field in line with the far field instead of on its own stream
+ * (every kernel then has the GPU to itself: isolated per-stage timings); default 0. */
+int fmmbem_op_set_serial(fmmbem_op* op, int serial);
 /* cumulative kernel launches issued by the op (graph kernel nodes included), number of
  * graph-launched applies, and the CUDA-event duration of the last fmmbem_op_gmres*
  * call (for the host variant: H2D of b .. D2H of x inclusive). */

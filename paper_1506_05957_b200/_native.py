@@ -61,6 +61,7 @@ SIGNATURES = {
                                               ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
                                               _c_double_p, _c_int32_p, _c_int32_p, _c_int32_p]),
     "fmmbem_op_set_timing": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int]),
+    "fmmbem_op_set_serial": (ctypes.c_int, [_vp, ctypes.c_int]),
     "fmmbem_op_stage_times": (ctypes.c_int, [_vp, _c_double_p, _c_int64_p, ctypes.c_int]),
     "fmmbem_op_counters": (ctypes.c_int, [_vp, _c_int64_p, _c_int64_p, _c_double_p]),
     "fmmbem_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),

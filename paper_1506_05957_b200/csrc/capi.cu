@@ -416,6 +416,13 @@ int fmmbem_op_set_timing(fmmbem_op* h, int enable, int use_graphs) {
   });
 }
 
+int fmmbem_op_set_serial(fmmbem_op* h, int serial) {
+  return guarded([&] {
+    FMM_REQUIRE(h, "null argument");
+    h->op->serial_near = serial != 0;
+  });
+}
+
 int fmmbem_op_stage_times(fmmbem_op* h, double* ms6, int64_t* calls, int reset) {
   return guarded([&] {
     FMM_REQUIRE(h, "null argument");

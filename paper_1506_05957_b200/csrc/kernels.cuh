@@ -65,14 +65,15 @@ inline int p2p_comps(P2PKind k) { return (k == P2PKind::LAP_Q || k == P2PKind::L
 // (start, count, tile offset) at their CSR position, and every item target's tile slot of
 // its own centroid Gauss point (-1 if not in the item) at its partial-sum position.
 struct LapdHdr {  // one P2P item in schedule (largest-first) order
-  int item, pair_begin, nl, ns, t0, nt, out_off, pad;
+  int item, pair_begin, nl, ns, t0, nt, out_off, nspec;
   double cx, cy, cz, pad2;  // target leaf centre
 };
 struct P2PAux {
   DevBuf<LapdHdr> hdr;
   int n_items = 0;
   DevBuf<int4> ltab;
-  DevBuf<int> slot;
+  DevBuf<int> slot;  // per item target: its own source's tile slot (own sources first), or -1
+  DevBuf<int> spec;  // per item: the own sources' positions in item (leaf) order, ascending
   int max_leaves = 1, max_tgt = 1;
   bool ready = false;
   void build(const Tree& S, const Tree& T, const std::vector<P2PItem>& items,

@@ -427,23 +427,28 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   const double* w = c.kind == K_LAP_SINGLE ? op.q.get() : c.kind == K_LAP_DOUBLE ? op.dip.get()
                                                                                 : op.wsrc.get();
   // near field on the second stream
-  FMM_CUDA(cudaEventRecord(op.ev_fork, s));
-  FMM_CUDA(cudaStreamWaitEvent(op.s_near, op.ev_fork, 0));
-  record(op, ST_P2P, false, op.s_near);
+  // near field on the second stream (concurrent with the far field), or in line
+  const bool serial = op.serial_near;
+  cudaStream_t sn = serial ? s : op.s_near;
+  if (!serial) {
+    FMM_CUDA(cudaEventRecord(op.ev_fork, s));
+    FMM_CUDA(cudaStreamWaitEvent(op.s_near, op.ev_fork, 0));
+  }
+  record(op, ST_P2P, false, sn);
   if (c.dense)
     launch_p2p((P2PKind)c.kind, S, T, op.dense_items.get(), (int)op.dense_items_h.size(),
-               op.dense_src.get(), op.dense_max_sources, w, op.part_dense.get(), op.s_near,
+               op.dense_src.get(), op.dense_max_sources, w, op.part_dense.get(), sn,
                nullptr);
   else if (sharded)
     launch_p2p((P2PKind)c.kind, S, T, sw.items.get(), (int)sw.items_h.size(), pl.p2p_src.get(),
-               sw.max_item_sources, w, op.part.get(), op.s_near, sw.p2p_order.get(), &sw.p2p_aux,
+               sw.max_item_sources, w, op.part.get(), sn, sw.p2p_order.get(), &sw.p2p_aux,
                op.p2p_sched.get(), op.srec.get());
   else
     launch_p2p((P2PKind)c.kind, S, T, pl.d_items.get(), (int)pl.items.size(), pl.p2p_src.get(),
-               op.max_item_sources, w, op.part.get(), op.s_near, pl.p2p_order.get(), &op.p2p_aux,
+               op.max_item_sources, w, op.part.get(), sn, pl.p2p_order.get(), &op.p2p_aux,
                op.p2p_sched.get(), op.srec.get());
-  record(op, ST_P2P, true, op.s_near);
-  FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
+  record(op, ST_P2P, true, sn);
+  if (!serial) FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
   // far field on the main stream
   if (!c.dense) {
     const double* q = (c.kind == K_LAP_SINGLE || c.kind == K_STOKESLET) ? op.q.get() : nullptr;
@@ -475,7 +480,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     record(op, ST_DOWN, false, s);  // (no L2L levels: the epilogue walks each leaf's path)
     record(op, ST_DOWN, true, s);
   }
-  FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
+  if (!serial) FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
   EpiArgs a;
   a.leaves = sharded ? sw.epi_leaves.get() : pl.tgt.leaves.get();
   a.item_begin = c.dense ? op.dense_item_begin.get() : sharded ? sw.item_begin.get() : pl.tleaf_item_begin.get();
@@ -555,7 +560,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
       clear_graphs(op);
       op.graph_sig = sig;
     }
-    const int key = p * 2 + (op.timing ? 1 : 0);
+    const int key = p * 4 + (op.timing ? 1 : 0) + (op.serial_near ? 2 : 0);
     auto it = op.graphs.find(key);
     if (it == op.graphs.end()) {
       cudaGraph_t g;

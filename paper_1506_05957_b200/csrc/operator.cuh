@@ -147,6 +147,7 @@ struct BemOp {
   cudaEvent_t call_ev[2] = {nullptr, nullptr};
   double last_call_ms = 0.0;
   bool use_graphs = true;
+  bool serial_near = false;  // near field in line with the far field (isolated kernel timings)
 
   // stage timing
   bool timing = false;

@@ -16,6 +16,8 @@
 // Stokes uses the direct stokeslet G f = f/r + r (r.f)/r^3 (kernels.py:42-48)
 // instead of the reference's four-channel decomposition of the near field;
 // the two agree to ~1e-13 and the direct form is cheaper.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "l2p.cuh"
 
@@ -211,20 +213,48 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 }
 
 struct LapdStage {  // shared-memory stage layout (offsets in bytes from the stage base)
-  size_t planes, tgt, ltab, slot, bytes;
+  size_t planes, tgt, ltab, slot, spec, bytes;
   __host__ __device__ LapdStage(int max_src, int max_leaves, int max_tgt) {
     planes = 0;
     tgt = (size_t)4 * max_src * sizeof(double2);        // [2][max_tgt] double2: (x', y'), (z', |t'|^2)
     ltab = tgt + (size_t)2 * max_tgt * sizeof(double2);
     slot = ltab + (size_t)max_leaves * sizeof(int4);
-    bytes = (slot + (size_t)max_tgt * sizeof(int) + 4 * sizeof(int) + 15) / 16 * 16;
+    spec = slot + (size_t)max_tgt * sizeof(int);
+    bytes = (spec + (size_t)max_tgt * sizeof(int) + 8 * sizeof(int) + 15) / 16 * 16;
   }
 };
+
+struct LapdSrc {
+  double2 ab, cs, dxy, dzs;  // (-2x', -2y'), (-2z', |s'|^2), (d_x, d_y), (d_z, -d.s')
+};
+
+__device__ __forceinline__ LapdSrc lapd_load(const double2* __restrict__ sh2, int max_src, int j) {
+  return LapdSrc{sh2[j], sh2[max_src + j], sh2[2 * max_src + j], sh2[3 * max_src + j]};
+}
+
+template <int TPT, bool MASK>
+__device__ __forceinline__ void lapd_body(const LapdSrc& u, int j, const double* tx, const double* ty,
+                                          const double* tz, const double* tt, const int* self,
+                                          double* acc) {
+#pragma unroll
+  for (int q = 0; q < TPT; ++q) {
+    double d2 = fma(tx[q], u.ab.x, fma(ty[q], u.ab.y, fma(tz[q], u.cs.x, u.cs.y + tt[q])));
+    // coincident pair: hi word of ~1e300 (the lo word is irrelevant), so r^-3 underflows to 0
+    if (MASK) d2 = __hiloint2double(j == self[q] ? 0x7E37E43C : __double2hiint(d2), __double2loint(d2));
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
+    const double y2 = y * y;
+    const double y3 = y2 * y;
+    const double e = fma(-d2, y2, 1.0);
+    const double rn = fma(u.dxy.x, tx[q], fma(u.dxy.y, ty[q], fma(u.dzs.x, tz[q], u.dzs.y)));
+    acc[q] = fma(rn, fma(1.5 * e, y3, y3), acc[q]);
+  }
+}
 
 template <int NCT, int NSTG>
 __global__ void __launch_bounds__(NCT + LAPD_PROD, 1)
 k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4* __restrict__ gl_ltab,
-           const int* __restrict__ gl_slot, int max_src, int max_leaves, int max_tgt,
+           const int* __restrict__ gl_slot, const int* __restrict__ gl_spec, int max_src, int max_leaves, int max_tgt,
            const double2* __restrict__ srec, double* __restrict__ part, unsigned* __restrict__ sched,
            long long* __restrict__ trace) {
   constexpr int TPT = LAPD_TPT, NPT = LAPD_PROD, ALL = NCT + NPT;
@@ -252,7 +282,8 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
       int4* ltab = reinterpret_cast<int4*>(base + L.ltab);
       int* slot = reinterpret_cast<int*>(base + L.slot);
       double2* tg = reinterpret_cast<double2*>(base + L.tgt);
-      int* hdr = slot + max_tgt;  // live (0: done), ns, nt, out_off
+      int* spec = slot + max_tgt;  // tile positions (item order) of the targets' own sources
+      int* hdr = spec + max_tgt;   // live (0: done), ns, nt, out_off, nspec
       if (pt == 0) TR(k, 0);
       if (k >= NSTG) bar_sync(BAR_EMPTY0 + st, ALL);
       if (pt == 0) TR(k, 1);
@@ -271,6 +302,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
       for (int q = pt; q < H.nl; q += NPT) ltab[q] = gl_ltab[H.pair_begin + q];
       for (int lt = pt; lt < H.nt; lt += NPT) {
         slot[lt] = gl_slot[H.out_off + lt];
+        if (lt < H.nspec) spec[lt] = gl_spec[H.out_off + lt];
         const double x = T.px[H.t0 + lt] - H.cx, y = T.py[H.t0 + lt] - H.cy, z = T.pz[H.t0 + lt] - H.cz;
         tg[lt] = make_double2(x, y);
         tg[max_tgt + lt] = make_double2(z, fma(x, x, fma(y, y, z * z)));
@@ -280,6 +312,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
         hdr[1] = H.ns;
         hdr[2] = H.nt;
         hdr[3] = H.out_off;
+        hdr[4] = H.nspec;
       }
       bar_sync(BAR_PROD, NPT);
       // flattened over the tile: 4 sources per thread per round, loads issued before use
@@ -304,14 +337,22 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
         for (int u = 0; u < 4; ++u) {
           const int i = i0 + u * NPT;
           if (i >= H.ns) break;
+          // destination: own sources first (rank among them), the rest compacted after
+          int r = 0, hi = H.nspec;  // r = number of own sources at tile positions < i
+          while (r < hi) {
+            const int mid = (r + hi) >> 1;
+            if (spec[mid] < i) r = mid + 1;
+            else hi = mid;
+          }
+          const int dst = (r < H.nspec && spec[r] == i) ? r : H.nspec + i - r;
           const double sx = v[u][0].x - H.cx, sy = v[u][0].y - H.cy, sz = v[u][1].x - H.cz;
           const double dx = v[u][1].y, dy = v[u][2].x, dz = v[u][2].y;
           const double ss = fma(sx, sx, fma(sy, sy, sz * sz));
           const double ds = fma(dx, sx, fma(dy, sy, dz * sz));
-          sh2[i] = make_double2(-2.0 * sx, -2.0 * sy);
-          sh2[max_src + i] = make_double2(-2.0 * sz, ss);
-          sh2[2 * max_src + i] = make_double2(dx, dy);
-          sh2[3 * max_src + i] = make_double2(dz, -ds);
+          sh2[dst] = make_double2(-2.0 * sx, -2.0 * sy);
+          sh2[max_src + dst] = make_double2(-2.0 * sz, ss);
+          sh2[2 * max_src + dst] = make_double2(dx, dy);
+          sh2[3 * max_src + dst] = make_double2(dz, -ds);
         }
       }
       if (pt == 0) TR(k, 2);
@@ -338,12 +379,12 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
     const double2* sh2 = reinterpret_cast<const double2*>(base);
     const int* slot = reinterpret_cast<const int*>(base + L.slot);
     const double2* tg = reinterpret_cast<const double2*>(base + L.tgt);
-    const int* hdr = slot + max_tgt;
+    const int* hdr = slot + 2 * max_tgt;
     if (threadIdx.x == 0) TR(k, 3);
     bar_sync(BAR_FULL0 + st, ALL);
     if (threadIdx.x == 0) TR(k, 4);
     if (hdr[0] == 0) break;
-    const int ns = hdr[1], nt = hdr[2], out_off = hdr[3];
+    const int ns = hdr[1], nt = hdr[2], out_off = hdr[3], nspec = hdr[4];
     // thread groups: nsl target slots (TPT targets each) x G source groups
     const int nsl = (nt + TPT - 1) / TPT;
     const int G = NCT / nsl;
@@ -362,22 +403,24 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
       self[q] = slot[lt];
     }
     if (g < G) {
-      for (int j = g; j < ns; j += G) {
-        const double2 ab = sh2[j], cs = sh2[max_src + j], dxy = sh2[2 * max_src + j],
-                      dzs = sh2[3 * max_src + j];
-#pragma unroll
-        for (int q = 0; q < TPT; ++q) {
-          double d2 = fma(tx[q], ab.x, fma(ty[q], ab.y, fma(tz[q], cs.x, cs.y + tt[q])));
-          // coincident pair: hi word of ~1e300 (the lo word is irrelevant)
-          d2 = __hiloint2double(j == self[q] ? 0x7E37E43C : __double2hiint(d2), __double2loint(d2));
-          double y;
-          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
-          const double y2 = y * y;
-          const double y3 = y2 * y;
-          const double e = fma(-d2, y2, 1.0);
-          const double rn = fma(dxy.x, tx[q], fma(dxy.y, ty[q], fma(dzs.x, tz[q], dzs.y)));
-          acc[q] = fma(rn, fma(1.5 * e, y3, y3), acc[q]);
+      // the self mask costs 2 issue slots per interaction: only the (at most TPT) iterations
+      // that meet a target's own source run the masked body; the loop is split around them
+      // the tile holds the item's targets' own sources first (j < nspec): only those iterations
+      // need the self mask (2 issue slots per interaction)
+      int j = g;
+      for (; j < nspec; j += G) lapd_body<TPT, true>(lapd_load(sh2, max_src, j), j, tx, ty, tz, tt, self, acc);
+      // software-pipelined: the next source's tile entry is read while this one is used
+      if (j < ns) {
+        LapdSrc u = lapd_load(sh2, max_src, j);
+        for (; j + G < ns; j += 2 * G) {
+          // two sources per trip: 2 TPT independent chains in flight
+          const LapdSrc v = lapd_load(sh2, max_src, j + G);
+          const LapdSrc w2 = lapd_load(sh2, max_src, min(j + 2 * G, ns - 1));
+          lapd_body<TPT, false>(u, j, tx, ty, tz, tt, self, acc);
+          lapd_body<TPT, false>(v, j + G, tx, ty, tz, tt, self, acc);
+          u = w2;
         }
+        if (j < ns) lapd_body<TPT, false>(u, j, tx, ty, tz, tt, self, acc);
       }
     }
     if (threadIdx.x == 0) TR(k, 5);
@@ -416,7 +459,8 @@ void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& ite
   std::vector<int4> lt(std::max<size_t>(p2p_src.size(), 1), make_int4(0, 0, 0, 0));
   int64_t part_len = 0;
   for (const auto& it : items) part_len = std::max<int64_t>(part_len, it.out_off + T.h_body_count[it.tgt_leaf]);
-  std::vector<int> sl(std::max<int64_t>(part_len, 1), -1);
+  std::vector<int> sl(std::max<int64_t>(part_len, 1), -1), sp(std::max<int64_t>(part_len, 1), 0);
+  std::vector<int> nspec_of(items.size(), 0);
   max_leaves = 1;
   max_tgt = 1;
   for (const auto& it : items) {
@@ -427,11 +471,18 @@ void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& ite
       off += S.h_body_count[leaf];
     }
     const int t0 = T.h_body_start[it.tgt_leaf], nt = T.h_body_count[it.tgt_leaf];
+    std::vector<std::pair<int, int>> own;  // (tile position, target)
     for (int l = 0; l < nt; ++l) {
       const int gs = self_src_sorted[t0 + l];
       for (int k = it.pair_begin; k < it.pair_end; ++k)
-        if (gs >= lt[k].x && gs < lt[k].x + lt[k].y) sl[it.out_off + l] = lt[k].z + gs - lt[k].x;
+        if (gs >= lt[k].x && gs < lt[k].x + lt[k].y) own.emplace_back(lt[k].z + gs - lt[k].x, l);
     }
+    std::sort(own.begin(), own.end());
+    for (size_t r = 0; r < own.size(); ++r) {
+      sl[it.out_off + own[r].second] = (int)r;  // the own source sits at tile slot r
+      sp[it.out_off + r] = own[r].first;
+    }
+    nspec_of[&it - items.data()] = (int)own.size();
     max_leaves = std::max(max_leaves, it.pair_end - it.pair_begin);
     max_tgt = std::max(max_tgt, nt);
   }
@@ -447,6 +498,7 @@ void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& ite
     e.t0 = T.h_body_start[it.tgt_leaf];
     e.nt = T.h_body_count[it.tgt_leaf];
     e.out_off = it.out_off;
+    e.nspec = nspec_of[ord[r]];
     e.cx = T.h_cx[it.tgt_leaf];
     e.cy = T.h_cy[it.tgt_leaf];
     e.cz = T.h_cz[it.tgt_leaf];
@@ -456,6 +508,7 @@ void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& ite
   hdr.upload(h, st);
   ltab.upload(lt, st);
   slot.upload(sl, st);
+  spec.upload(sp, st);
   ready = true;
 }
 
@@ -488,7 +541,8 @@ void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const dou
   FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = std::min(aux.n_items, sms);
   if (grid > 0)
-    kern<<<grid, nthr, smem, st>>>(T, aux.hdr.get(), aux.n_items, aux.ltab.get(), aux.slot.get(), max_src,
+    kern<<<grid, nthr, smem, st>>>(T, aux.hdr.get(), aux.n_items, aux.ltab.get(), aux.slot.get(),
+                                   aux.spec.get(), max_src,
                                    aux.max_leaves, aux.max_tgt, srec, part, sched, p2p_trace_buffer());
   FMM_LAUNCH_CHECK();
 }

@@ -333,6 +333,10 @@ class GpuBemOperator:
     def set_timing(self, enable: bool, use_graphs: bool = True):
         N.check(self._lib.fmmbem_op_set_timing(self._h, 1 if enable else 0, 1 if use_graphs else 0))
 
+    def set_serial(self, serial: bool):
+        """Run the near field in line with the far field (isolated kernel timings)."""
+        N.check(self._lib.fmmbem_op_set_serial(self._h, 1 if serial else 0))
+
     # -- multi-GPU ---------------------------------------------------------------
     def leaf_work(self, which: str = "tgt") -> np.ndarray:
         """Per-leaf work weights (body order) used to partition the leaves across ranks."""

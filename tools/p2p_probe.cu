@@ -12,7 +12,9 @@
 
 constexpr int NSRC = 512;
 
-template <int TPT>
+// MODE 0: production loop; 1: no self mask; 2: fp32 seed (F2F + MUFU.RSQ + F2F) instead of
+// MUFU.RSQ64H; 3: no mask, seed = rsqrt of the previous source's d2 (no MUFU in the chain)
+template <int TPT, int MODE = 0>
 __global__ void lapd_loop(const double2* __restrict__ src, int reps, double* out) {
   __shared__ double2 sh[4 * NSRC];
   for (int i = threadIdx.x; i < 4 * NSRC; i += blockDim.x) sh[i] = src[i];
@@ -35,9 +37,11 @@ __global__ void lapd_loop(const double2* __restrict__ src, int reps, double* out
 #pragma unroll
       for (int q = 0; q < TPT; ++q) {
         double d2 = fma(tx[q], ab.x, fma(ty[q], ab.y, fma(tz[q], cs.x, cs.y + tt[q])));
-        d2 = __hiloint2double(j == self[q] ? 0x7E37E43C : __double2hiint(d2), __double2loint(d2));
+        if (MODE == 0 || MODE == 2)
+          d2 = __hiloint2double(j == self[q] ? 0x7E37E43C : __double2hiint(d2), __double2loint(d2));
         double y;
-        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
+        if (MODE == 2) y = (double)rsqrtf((float)d2);
+        else asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
         const double y2 = y * y;
         const double y3 = y2 * y;
         const double e = fma(-d2, y2, 1.0);
@@ -72,18 +76,36 @@ __global__ void mufu_lat(double* out, int n) {
   if (threadIdx.x == 0) { out[0] = (double)(t1 - t0) / n; out[1] = x; }
 }
 
-template <int TPT>
+__global__ void mufu_tput(double* out, int n) {
+  double x0 = 1.0 + threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  double a = 0;
+  for (int i = 0; i < n; ++i) {
+    double y0, y1, y2, y3, y4, y5, y6, y7;
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x0));
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y1) : "d"(x1));
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y2) : "d"(x2));
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y3) : "d"(x3));
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y4) : "d"(x4));
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y5) : "d"(x5));
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y6) : "d"(x6));
+    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y7) : "d"(x7));
+    a += y0 + y1 + y2 + y3 + y4 + y5 + y6 + y7;
+  }
+  if (a == 1.2345) out[0] = a;
+}
+
+template <int TPT, int MODE = 0>
 int run(const double2* src, double* out, int sms, int threads, int ctas_per_sm, double clk_ghz) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int blocks = sms * ctas_per_sm, reps = 16;
-  lapd_loop<TPT><<<blocks, threads>>>(src, 1, out);
+  lapd_loop<TPT, MODE><<<blocks, threads>>>(src, 1, out);
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
   for (int r = 0; r < 3; ++r) {
     cudaEventRecord(e0);
-    lapd_loop<TPT><<<blocks, threads>>>(src, reps, out);
+    lapd_loop<TPT, MODE><<<blocks, threads>>>(src, reps, out);
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -91,13 +113,13 @@ int run(const double2* src, double* out, int sms, int threads, int ctas_per_sm, 
     best = ms < best ? ms : best;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lapd_loop<TPT>, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lapd_loop<TPT, MODE>, threads, 0);
   const double inter = (double)blocks * threads * TPT * (NSRC / 8) * reps;
   const double dp = inter * 13.0;
   const double peak_dp = sms * 64.0 * clk_ghz * 1e9;
-  printf("{\"tpt\": %d, \"threads\": %d, \"ctas_per_sm\": %d, \"resident\": %d, \"ginter_per_s\": %.2f, "
+  printf("{\"mode\": %d, \"tpt\": %d, \"threads\": %d, \"ctas_per_sm\": %d, \"resident\": %d, \"ginter_per_s\": %.2f, "
          "\"alg_tflops\": %.2f, \"dp_pipe_frac\": %.3f}\n",
-         TPT, threads, ctas_per_sm, occ, inter / (best * 1e-3) / 1e9, 18.0 * inter / (best * 1e-3) / 1e12,
+         MODE, TPT, threads, ctas_per_sm, occ, inter / (best * 1e-3) / 1e9, 18.0 * inter / (best * 1e-3) / 1e12,
          dp / (best * 1e-3) / peak_dp);
   return 0;
 }
@@ -122,10 +144,25 @@ int main() {
   CK(cudaMemcpy(lat, out, 16, cudaMemcpyDeviceToHost));
   printf("{\"rsq64h_plus_dadd_latency_cycles\": %.2f}\n", lat[0]);
   const double clk = 1.965;
-  for (int c : {1, 2, 3, 4}) run<4>(src, out, sms, 256, c, clk);
-  for (int c : {2, 3, 4, 6}) run<2>(src, out, sms, 256, c, clk);
-  for (int c : {1, 2, 3}) run<6>(src, out, sms, 256, c, clk);
-  for (int c : {1, 2}) run<8>(src, out, sms, 256, c, clk);
-  for (int c : {2, 4}) run<4>(src, out, sms, 128, c, clk);
+  {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    mufu_tput<<<sms * 4, 256>>>(out, 16);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    mufu_tput<<<sms * 4, 256>>>(out, 2048);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double n = 8.0 * 2048 * sms * 4 * 256;
+    printf("{\"rsq64h_per_clk_per_sm\": %.2f}\n", n / (ms * 1e-3) / (sms * clk * 1e9));
+  }
+  for (int c : {1, 3}) run<4, 0>(src, out, sms, 256, c, clk);
+  for (int c : {1, 3}) run<4, 1>(src, out, sms, 256, c, clk);
+  for (int c : {1, 3}) run<4, 2>(src, out, sms, 256, c, clk);
+  for (int c : {1, 2}) run<8, 0>(src, out, sms, 256, c, clk);
+  for (int c : {1, 2}) run<8, 1>(src, out, sms, 256, c, clk);
   return 0;
 }

@@ -28,23 +28,24 @@ lib.fmmbem_debug_p2p_trace.restype = ctypes.c_int
 lib.fmmbem_debug_p2p_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_int64(buf.size))
 t = buf.reshape(1024, 32, 8)
 ctas = [c for c in range(1024) if t[c, 0, 3] != 0]
-tot = {k: 0 for k in ("p_wait", "p_stage", "c_wait", "c_loop0", "c_looplast", "c_red", "span")}
+tot = {k: 0 for k in ("p_wait", "p_stage", "c_starve0", "c_starve", "c_busy", "span", "items")}
 for c in ctas:
-    items = [k for k in range(32) if t[c, k, 4] != 0]
-    start = t[c, 0, 3]
-    end = max(t[c, k, 7] for k in items if t[c, k, 7] != 0) if items else start
-    tot["span"] += end - start
+    items = [k for k in range(32) if t[c, k, 0] != 0 and t[c, k, 2] != 0]
+    if not items:
+        continue
+    start = t[c, 0, 0]
+    ends = [t[c, k, 7] for k in items]
+    tot["span"] += max(ends) - start
+    tot["items"] += len(items)
+    prev_end = start
     for k in items:
-        if t[c, k, 0]:
-            tot["p_wait"] += t[c, k, 1] - t[c, k, 0]
-            if t[c, k, 2]:
-                tot["p_stage"] += t[c, k, 2] - t[c, k, 1]
-        tot["c_wait"] += t[c, k, 4] - t[c, k, 3]
-        if t[c, k, 5]:
-            tot["c_loop0"] += t[c, k, 5] - t[c, k, 4]
-            tot["c_looplast"] += t[c, k, 6] - t[c, k, 4]
-            tot["c_red"] += t[c, k, 7] - t[c, k, 5]
+        tot["p_wait"] += t[c, k, 1] - t[c, k, 0]
+        tot["p_stage"] += t[c, k, 2] - t[c, k, 1]
+        starve = max(0, t[c, k, 2] - prev_end)  # consumers idle until the producer staged item k
+        tot["c_starve0" if k == 0 else "c_starve"] += starve
+        tot["c_busy"] += t[c, k, 7] - max(prev_end, t[c, k, 2])
+        prev_end = t[c, k, 7]
 n = max(len(ctas), 1)
 print(name, p, "ctas", len(ctas), {k: round(v / n) for k, v in tot.items()})
-for c in ctas[:2]:
-    print("cta", c, [list(map(int, t[c, k] - t[c, 0, 3])) for k in range(8) if t[c, k, 3]])
+last = sorted(((c, [int(t[c, k, 2] - t[c, k, 1]) for k in range(32) if t[c, k, 2]]) for c in ctas[:1]))
+print("producer stage cycles per item (cta 0):", last)
