@@ -78,4 +78,60 @@ __device__ __forceinline__ void l2p_eval(const double2* __restrict__ L, int H, i
   }
 }
 
+// One-channel potential-only L2P for 4 column slices (warp-uniform): slice k evaluates the
+// columns m with (m mod 8) in {k, 7 - k} (column m has p + 1 - m terms: near-equal shares).
+// Each column starts from R_m^m = c_m (x + i y)^m, c_m = prod_{j <= m} -1/(2j)
+// (harmonics.py:50-52), by binary powering, and runs the n-recurrence with the coefficients
+// (2n-1)/((n+m)(n-m)) and 1/((n+m)(n-m)) from constant memory (warp-uniform (n, m)).
+struct L2PConst {
+  double diag[P_MAX + 1];
+  double ra[(P_MAX + 1) * (P_MAX + 1)];  // [n][m] (2n - 1) / ((n + m)(n - m))
+  double rb[(P_MAX + 1) * (P_MAX + 1)];  // [n][m] 1 / ((n + m)(n - m))
+};
+// (one copy per translation unit: no relocatable device code; operator.cu uploads its own)
+static __constant__ L2PConst c_l2p;
+
+__device__ __forceinline__ double2 cpow_int(double2 w, int m) {
+  double2 r = make_double2(1.0, 0.0);
+  while (m) {
+    if (m & 1) r = cmul(r, w);
+    m >>= 1;
+    if (m) w = cmul(w, w);
+  }
+  return r;
+}
+
+__device__ __forceinline__ double l2p_eval1(const double2* __restrict__ L, int p, double x, double y,
+                                            double z, int slice) {
+  const double rho2 = x * x + y * y + z * z;
+  const double2 w = make_double2(x, y);
+  double acc = 0.0;
+  for (int m0 = 0; m0 <= p; m0 += 8) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = m0 + (h ? 7 - slice : slice);
+      if (m > p) continue;
+      double2 cur = cscale(cpow_int(w, m), c_l2p.diag[m]), prev2 = make_double2(0.0, 0.0);
+      int i = hidx(m, m);
+      double col = fma(L[i].x, cur.x, -L[i].y * cur.y);
+      if (m < p) {
+        prev2 = cur;
+        cur = cscale(cur, z);
+        i += m + 1;
+        col = fma(L[i].x, cur.x, fma(-L[i].y, cur.y, col));
+      }
+      for (int n = m + 2; n <= p; ++n) {
+        const double az = c_l2p.ra[n * (P_MAX + 1) + m] * z, b = c_l2p.rb[n * (P_MAX + 1) + m] * rho2;
+        const double2 nx = make_double2(fma(az, cur.x, -b * prev2.x), fma(az, cur.y, -b * prev2.y));
+        prev2 = cur;
+        cur = nx;
+        i += n;
+        col = fma(L[i].x, cur.x, fma(-L[i].y, cur.y, col));
+      }
+      acc = m == 0 ? acc + col : fma(2.0, col, acc);
+    }
+  }
+  return acc;
+}
+
 }  // namespace fmmbem

@@ -18,6 +18,22 @@ namespace fmmbem {
 
 void upload_index_tables();
 
+void upload_l2p_constants() {
+  static bool done = false;
+  if (done) return;
+  static L2PConst h;
+  h.diag[0] = 1.0;
+  for (int m = 1; m <= P_MAX; ++m) h.diag[m] = h.diag[m - 1] * (-1.0 / (2.0 * m));
+  for (int n = 0; n <= P_MAX; ++n)
+    for (int m = 0; m <= P_MAX; ++m) {
+      const double d = (double)(n + m) * (double)(n - m);
+      h.ra[n * (P_MAX + 1) + m] = (n >= m + 2) ? (2.0 * n - 1.0) / d : 0.0;
+      h.rb[n * (P_MAX + 1) + m] = (n >= m + 2) ? 1.0 / d : 0.0;
+    }
+  FMM_CUDA(cudaMemcpyToSymbol(c_l2p, &h, sizeof(h)));
+  done = true;
+}
+
 namespace {
 
 constexpr double FOUR_PI = 12.566370614359172;
@@ -170,9 +186,13 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
       if (valid)
         for (int k = 0; k < np; ++k) {
           const int cell = a.path[pb + k];
-          l2p_eval<C, Tr::GRAD>(sL + (size_t)k * C * H, H, a.p, T.px[ti] - T.cx[cell],
-                                T.py[ti] - T.cy[cell], T.pz[ti] - T.cz[cell], pot, grad, T.rec,
-                                slice, NS);
+          if (C == 1)
+            pot[0] += l2p_eval1(sL + (size_t)k * H, a.p, T.px[ti] - T.cx[cell], T.py[ti] - T.cy[cell],
+                                T.pz[ti] - T.cz[cell], slice);
+          else
+            l2p_eval<C, Tr::GRAD>(sL + (size_t)k * C * H, H, a.p, T.px[ti] - T.cx[cell],
+                                  T.py[ti] - T.cy[cell], T.pz[ti] - T.cz[cell], pot, grad, T.rec,
+                                  slice, NS);
         }
     }
     if (KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) {
@@ -338,6 +358,7 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   FMM_REQUIRE(formulation >= 0 && formulation <= 2, "unknown formulation");
   FMM_REQUIRE(n_gauss_singular >= 1, "n_gauss_singular must be >= 1");
   upload_index_tables();
+  upload_l2p_constants();
   op.formulation = formulation;
   op.mu = mu;
   op.near_factor = near_factor;
