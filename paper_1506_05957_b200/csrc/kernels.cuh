@@ -45,7 +45,7 @@ void build_rot_aux(const double* geo, int n_off, int P, double* aux, cudaStream_
 void build_rot_frag(const double* rot, int n_off, int P, double* out, cudaStream_t s);
 void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
                     int C, const double2* M, double2* pout, cudaStream_t st);
-constexpr int M2L_ROT_MIN_P = 6;  // rotation-based M2L from this order up
+constexpr int M2L_ROT_MIN_P = 3;  // rotation-based M2L from this order up
 // M2M through octant-grouped child translations (cout: per-cell child contributions)
 void launch_m2m_grouped(const Plan& plan, int p, int C, const double2* rfull, double2* M,
                         double2* cout, cudaStream_t st);
