@@ -10,7 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 python tools/launch_summary.py gpurun_out/launches.csv --tail 200 | head -25
 if [ "${FULL:-1}" = 1 ]; then
-ncu --set full --clock-control none --import-source on -k regex:"k_p2p|k_m2l_rot|k_p2m_basis|k_epilogue|k_arnoldi" \
+ncu --set full --clock-control none --import-source on -k regex:"k_p2p|k_m2l_rot|k_p2m_basis|k_epilogue|k_arnoldi|k_m2l_gather" \
     --launch-skip 10 -c 8 -o gpurun_out/full -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 echo "ncu full exit $?"
 fi
