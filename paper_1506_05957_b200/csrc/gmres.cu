@@ -177,6 +177,79 @@ __global__ void __launch_bounds__(RT) k_arnoldi(int64_t n, int k, const double* 
   for (int64_t i = i0; i < n; i += stride) w[i] = xnext[i] = h > 0.0 ? w[i] / h : 0.0;
 }
 
+// The same Arnoldi step for n <= ACL * ACT * AE on one thread-block cluster: w stays in
+// registers (AE elements per thread), each sweep's CTA partials are exchanged through
+// distributed shared memory and added in rank order by every CTA (bitwise-identical h_j),
+// so a sweep costs one cluster barrier instead of a grid-wide one.
+constexpr int ACL = 8;     // CTAs per cluster (portable size)
+constexpr int ACT = 1024;  // threads per CTA
+constexpr int AE = 4;      // elements per thread: n <= 32 768
+
+__global__ void __launch_bounds__(ACT) k_arnoldi_cluster(int n, int k, const double* __restrict__ V,
+                                                         const double* __restrict__ w0, double* w,
+                                                         double* xnext, double* hd, double* mbox,
+                                                         unsigned long long* mflag,
+                                                         unsigned long long seq) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double sh[ACT / 32];
+  __shared__ double part[2 * ACL];
+  const int rank = (int)cluster.block_rank();
+  const int t = rank * ACT + threadIdx.x;  // element t + e * ACL * ACT
+  // registers: w, the current basis vector v_j (v_{j-1} of the next sweep) and v_{j+1},
+  // prefetched before the sweep's cluster barrier
+  double wr[AE], vc[AE], vn[AE];
+#pragma unroll
+  for (int e = 0; e < AE; ++e) {
+    const int i = t + e * ACL * ACT;
+    wr[e] = i < n ? w0[i] : 0.0;
+    vn[e] = i < n ? V[i] : 0.0;
+  }
+  double h = 0.0;
+  for (int j = 0; j <= k + 1; ++j) {
+    double acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < AE; ++e) {
+      if (j) wr[e] = fma(-h, vc[e], wr[e]);  // w -= h_{j-1} v_{j-1}
+      vc[e] = vn[e];
+    }
+    if (j + 1 <= k) {
+#pragma unroll
+      for (int e = 0; e < AE; ++e) {
+        const int i = t + e * ACL * ACT;
+        vn[e] = i < n ? V[(size_t)(j + 1) * n + i] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < AE; ++e) acc = j <= k ? fma(vc[e], wr[e], acc) : fma(wr[e], wr[e], acc);
+    const double bs = block_sum(acc, sh);
+    // push this CTA's partial into every CTA's slot [j & 1][rank] (remote stores are
+    // posted; the barrier's release/acquire makes them visible), then read locally
+    if (threadIdx.x == 0)  // (block_sum's total lives in thread 0)
+#pragma unroll
+      for (int r = 0; r < ACL; ++r) *cluster.map_shared_rank(part + (j & 1) * ACL + rank, r) = bs;
+    cluster.sync();
+    double tot = 0.0;
+#pragma unroll
+    for (int r = 0; r < ACL; ++r) tot += part[(j & 1) * ACL + r];
+    h = j > k ? sqrt(tot) : tot;
+    if (t == 0) {
+      hd[j] = h;
+      mbox[j] = h;
+    }
+  }
+  if (t == 0) {  // the column is complete: post it to the host
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(mflag) = seq;
+  }
+#pragma unroll
+  for (int e = 0; e < AE; ++e) {
+    const int i = t + e * ACL * ACT;
+    if (i < n) w[i] = xnext[i] = h > 0.0 ? wr[e] / h : 0.0;
+  }
+  cluster.sync();  // no CTA may exit while others still read its shared memory
+}
+
 double relax_eps(double r, double eta) { return std::min(eta / std::min(std::max(r, eta), 1.0), 1.0); }
 
 int schedule_p(double r, double eta, int p_initial, int p_min) {
@@ -271,8 +344,23 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
       unsigned long long sq = ++op.mbox_seq;
       const double* w0 = op.y_out.get();
       double* xn = op.x_in.get();
-      void* args[] = {&nn, &kk, &Vc, &w0, &w, &xn, &pp, &hd, &mb, &mf, &sq};
-      FMM_CUDA(cudaLaunchCooperativeKernel((const void*)k_arnoldi, dim3(AB), dim3(RT), args, 0, s));
+      if (n <= (int64_t)ACL * ACT * AE) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ACL);
+        cfg.blockDim = dim3(ACT);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ACL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        FMM_CUDA(cudaLaunchKernelEx(&cfg, k_arnoldi_cluster, (int)n, kk, Vc, w0, w, xn, hd, mb, mf, sq));
+      } else {
+        void* args[] = {&nn, &kk, &Vc, &w0, &w, &xn, &pp, &hd, &mb, &mf, &sq};
+        FMM_CUDA(cudaLaunchCooperativeKernel((const void*)k_arnoldi, dim3(AB), dim3(RT), args, 0, s));
+      }
     }
     FMM_LAUNCH_CHECK();
     op.kernel_launches += 1;
