@@ -52,11 +52,11 @@ __device__ void finish(double part, double* partials, unsigned* counter, double*
   if (threadIdx.x == 0) {
     *out = do_sqrt ? sqrt(t) : t;
     *counter = 0u;
-    if (mflag) {
+    if (mbox) {
       mbox[0] = *out;
       __threadfence_system();
-      *reinterpret_cast<volatile unsigned long long*>(mflag) = seq;
     }
+    if (mflag) *reinterpret_cast<volatile unsigned long long*>(mflag) = seq;
   }
 }
 
@@ -118,7 +118,7 @@ __global__ void k_combine(int64_t n, int m, const double* __restrict__ V, const 
 __global__ void k_scale(int64_t n, const double* b, const double* nb, double* v, double* v2) {
   const double d = *nb;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    v[i] = v2[i] = b[i] / d;
+    v[i] = v2[i] = d > 0.0 ? b[i] / d : 0.0;  // (b = 0: the host returns x = 0 after the first column)
 }
 
 // One Arnoldi step in a single cooperative launch (grid-wide barriers between
@@ -250,6 +250,36 @@ __global__ void __launch_bounds__(ACT) k_arnoldi_cluster(int n, int k, const dou
   cluster.sync();  // no CTA may exit while others still read its shared memory
 }
 
+// ||b|| on one cluster (n <= ACL * ACT * AE): written to the device scalar and posted to the
+// host mailbox slot, read by the host together with the first Arnoldi column
+__global__ void __launch_bounds__(ACT) k_norm_cluster(int n, const double* __restrict__ b, double* out,
+                                                      double* mbox) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double sh[ACT / 32];
+  __shared__ double part[ACL];
+  const int rank = (int)cluster.block_rank();
+  const int t = rank * ACT + threadIdx.x;
+  double acc = 0.0;
+#pragma unroll
+  for (int e = 0; e < AE; ++e) {
+    const int i = t + e * ACL * ACT;
+    if (i < n) acc = fma(b[i], b[i], acc);
+  }
+  const double bs = block_sum(acc, sh);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int r = 0; r < ACL; ++r) *cluster.map_shared_rank(part + rank, r) = bs;
+  cluster.sync();
+  if (t == 0) {
+    double tot = 0.0;
+#pragma unroll
+    for (int r = 0; r < ACL; ++r) tot += part[r];
+    *out = mbox[0] = sqrt(tot);
+    __threadfence_system();
+  }
+}
+
 double relax_eps(double r, double eta) { return std::min(eta / std::min(std::max(r, eta), 1.0), 1.0); }
 
 int schedule_p(double r, double eta, int p_initial, int p_min) {
@@ -303,20 +333,47 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
       }
     }
   };
-  // ||b||
+  // ||b||: device scalar for k_scale, and mailbox slot max_iter + 2 for the host, read with the
+  // first Arnoldi column (no round trip before the first mat-vec)
   double* nb = scal.get() + max_iter + 2;
-  const unsigned long long seq_b = ++op.mbox_seq;
-  k_norm<<<RB, RT, 0, s>>>(n, const_cast<double*>(b), nullptr, nullptr, partials.get(), counter.get(), nb,
-                           op.mbox_d, op.mflag_d, seq_b);
+  double* nb_box = op.mbox_d + max_iter + 2;
+  auto cluster_cfg = [&](cudaLaunchAttribute* at) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ACL);
+    cfg.blockDim = dim3(ACT);
+    cfg.stream = s;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ACL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cfg;
+  };
+  if (n <= (int64_t)ACL * ACT * AE) {
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = cluster_cfg(at);
+    FMM_CUDA(cudaLaunchKernelEx(&cfg, k_norm_cluster, (int)n, b, nb, nb_box));
+  } else {
+    k_norm<<<RB, RT, 0, s>>>(n, const_cast<double*>(b), nullptr, nullptr, partials.get(), counter.get(), nb,
+                             nb_box, nullptr, 0);
+  }
   FMM_LAUNCH_CHECK();
   op.kernel_launches += 1;
-  wait_post(seq_b);
-  const double norm_b = op.mbox_h[0];
-  if (norm_b == 0.0) {
-    FMM_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  double norm_b = -1.0;  // known after the first column
+  auto read_norm_b = [&]() {
+    norm_b = op.mbox_h[max_iter + 2];
+    if (norm_b == 0.0) {
+      FMM_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+      FMM_CUDA(cudaStreamSynchronize(s));
+      res.converged = true;
+      return true;
+    }
+    return false;
+  };
+  if (max_iter == 0) {
     FMM_CUDA(cudaStreamSynchronize(s));
-    res.converged = true;
-    return res;
+    if (read_norm_b()) return res;
   }
   DevBuf<double>& V = op.g_basis;
   V.ensure((size_t)(max_iter + 1) * n);
@@ -325,7 +382,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   std::vector<double> H((size_t)(max_iter + 1) * std::max(max_iter, 1), 0.0);
   auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * max_iter + j]; };
   std::vector<double> cs(max_iter), sn(max_iter), g(max_iter + 1, 0.0), hcol(max_iter + 2);
-  g[0] = norm_b;
+  if (norm_b > 0.0) g[0] = norm_b;
   double residual = 1.0;
   int prev_p = p_initial;
   double* hd = scal.get();  // H column k on device: hd[0..k+1]
@@ -345,17 +402,8 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
       const double* w0 = op.y_out.get();
       double* xn = op.x_in.get();
       if (n <= (int64_t)ACL * ACT * AE) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(ACL);
-        cfg.blockDim = dim3(ACT);
-        cfg.stream = s;
         cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = ACL;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cudaLaunchConfig_t cfg = cluster_cfg(at);
         FMM_CUDA(cudaLaunchKernelEx(&cfg, k_arnoldi_cluster, (int)n, kk, Vc, w0, w, xn, hd, mb, mf, sq));
       } else {
         void* args[] = {&nn, &kk, &Vc, &w0, &w, &xn, &pp, &hd, &mb, &mf, &sq};
@@ -365,6 +413,10 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     FMM_LAUNCH_CHECK();
     op.kernel_launches += 1;
     wait_post(op.mbox_seq);
+    if (k == 0) {
+      if (read_norm_b()) return res;
+      g[0] = norm_b;
+    }
     for (int j = 0; j <= k + 1; ++j) hcol[j] = op.mbox_h[j];
     if (op.timing) {
       FMM_CUDA(cudaStreamSynchronize(s));
