@@ -81,12 +81,15 @@ struct P2PAux {
 };
 // aux (LAP_D) selects the persistent expanded-form double-layer kernel, which also needs a
 // 2-uint schedule counter (zero before the first launch; self-resetting) and the sources as
-// records srec[3 i .. 3 i + 2] = (x, y), (z, d_x), (d_y, d_z) in sorted order; without them, or
+// static records srec[3 i .. 3 i + 2] = (x, y), (z, w n_x), (w n_y, w n_z) in sorted order with
+// the panel s_panel[i] whose density x[panel] scales the dipole; without them, or
 // when the stages do not fit shared memory, the difference-form kernel runs.
 void launch_p2p(P2PKind kind, const TreeDev& S, const TreeDev& T, const P2PItem* items,
                 int n_items, const int* p2p_src, int max_sources, const double* w, double* part,
                 cudaStream_t st, const int* order, const P2PAux* aux = nullptr,
-                unsigned* sched = nullptr, const double2* srec = nullptr);
+                unsigned* sched = nullptr, const double2* srec = nullptr,
+                const int* s_panel = nullptr, const double* x = nullptr);
+bool p2p_lapd_usable(const P2PAux* aux, int max_sources);
 
 // generic channel near field (FmmPlan.near_field): charges q[C][ns] and/or dipoles d[C][ns][3];
 // accumulates into pot[C][nt] (+ grad[C][nt][3]) in ORIGINAL target order.

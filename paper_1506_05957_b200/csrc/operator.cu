@@ -49,6 +49,18 @@ __global__ void k_sorted_sources(int64_t ns, const int* perm, const double* gw, 
   if (o % 4 == 0) self_src[tgt_perm_inv[o / 4]] = (int)i;
 }
 
+// double-layer near-field source records (x, y), (z, w n_x), (w n_y, w n_z), sorted order
+__global__ void k_source_records(int64_t ns, const double* px, const double* py, const double* pz,
+                                 const double* s_w, const int* s_panel, const double* nrm, double2* srec) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ns) return;
+  const double w = s_w[i];
+  const int pn = s_panel[i];
+  srec[3 * i] = make_double2(px[i], py[i]);
+  srec[3 * i + 1] = make_double2(pz[i], w * nrm[3 * pn]);
+  srec[3 * i + 2] = make_double2(w * nrm[3 * pn + 1], w * nrm[3 * pn + 2]);
+}
+
 __global__ void k_invert_perm(int64_t n, const int* perm, int* inv) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) inv[perm[i]] = (int)i;
@@ -59,8 +71,7 @@ template <int KIND>
 __global__ void k_density(int64_t ns, const double* __restrict__ s_w, const int* __restrict__ s_panel,
                           const double* __restrict__ px, const double* __restrict__ py,
                           const double* __restrict__ pz, const double* __restrict__ nrm,
-                          const double* __restrict__ x, double* q, double* dip, double* wsrc,
-                          double2* __restrict__ srec) {
+                          const double* __restrict__ x, double* q, double* dip, double* wsrc) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= ns) return;
   const int pn = s_panel[i];
@@ -73,10 +84,6 @@ __global__ void k_density(int64_t ns, const double* __restrict__ s_w, const int*
     dip[3 * i] = d0;
     dip[3 * i + 1] = d1;
     dip[3 * i + 2] = d2;
-    // the near field's source records (x, y), (z, d_x), (d_y, d_z)
-    srec[3 * i] = make_double2(px[i], py[i]);
-    srec[3 * i + 1] = make_double2(pz[i], d0);
-    srec[3 * i + 2] = make_double2(d1, d2);
   } else {
     const double f0 = w * x[3 * pn], f1 = w * x[3 * pn + 1], f2 = w * x[3 * pn + 2];
     const double yf = px[i] * f0 + py[i] * f1 + pz[i] * f2;
@@ -254,7 +261,7 @@ void launch_density(BemOp& op, const double* x, cudaStream_t s) {
   const int64_t ns = op.plan.src.n_points;
   k_density<KIND><<<grid_for(ns, 256), 256, 0, s>>>(
       ns, op.s_weight.get(), op.s_panel.get(), op.plan.src.px.get(), op.plan.src.py.get(),
-      op.plan.src.pz.get(), op.normal.get(), x, op.q.get(), op.dip.get(), op.wsrc.get(), op.srec.get());
+      op.plan.src.pz.get(), op.normal.get(), x, op.q.get(), op.dip.get(), op.wsrc.get());
   FMM_LAUNCH_CHECK();
 }
 
@@ -311,7 +318,6 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
   op.q.ensure((size_t)ns * (kind == K_STOKESLET ? 4 : 1));
   op.dip.ensure((size_t)ns * 3 * (kind == K_STRESSLET ? 7 : 1));
   op.wsrc.ensure((size_t)ns * 6);
-  op.srec.ensure((size_t)ns * 3);
   if (dense) {
     ensure_dense(op);
     op.part_dense.ensure((size_t)std::max<int64_t>(op.dense_part_len, 1) * 3);
@@ -407,6 +413,11 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
                                                         op.s_weight.get(), op.s_panel.get(), tinv.get(),
                                                         op.self_src.get());
     FMM_LAUNCH_CHECK();
+    op.srec.resize((size_t)ns * 3);
+    k_source_records<<<grid_for(ns, 256), 256, 0, s>>>(ns, op.plan.src.px.get(), op.plan.src.py.get(),
+                                                        op.plan.src.pz.get(), op.s_weight.get(),
+                                                        op.s_panel.get(), op.normal.get(), op.srec.get());
+    FMM_LAUNCH_CHECK();
     FMM_CUDA(cudaStreamSynchronize(s));
     op.h_self_src = op.self_src.download(s);
   }
@@ -439,7 +450,14 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   const int C = layer_channels(c.kind);
   const TreeDev S = tree_dev(pl.src), T = tree_dev(pl.tgt);
   record(op, ST_TOTAL, false, s);
-  switch (c.kind) {
+  // the double layer's persistent near field reads x through static source records and the
+  // basis upward pass reads x directly: the Gauss-point densities are only needed otherwise
+  const bool basis_up = c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p;
+  const bool lapd_near = c.kind == K_LAP_DOUBLE && !c.dense &&
+                         p2p_lapd_usable(sharded ? &sw.p2p_aux : &op.p2p_aux,
+                                         sharded ? sw.max_item_sources : op.max_item_sources);
+  const bool need_density = !(lapd_near && basis_up);
+  if (need_density) switch (c.kind) {
     case K_LAP_SINGLE: launch_density<K_LAP_SINGLE>(op, c.x, s); break;
     case K_LAP_DOUBLE: launch_density<K_LAP_DOUBLE>(op, c.x, s); break;
     case K_STOKESLET: launch_density<K_STOKESLET>(op, c.x, s); break;
@@ -463,11 +481,11 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   else if (sharded)
     launch_p2p((P2PKind)c.kind, S, T, sw.items.get(), (int)sw.items_h.size(), pl.p2p_src.get(),
                sw.max_item_sources, w, op.part.get(), sn, sw.p2p_order.get(), &sw.p2p_aux,
-               op.p2p_sched.get(), op.srec.get());
+               op.p2p_sched.get(), op.srec.get(), op.s_panel.get(), c.x);
   else
     launch_p2p((P2PKind)c.kind, S, T, pl.d_items.get(), (int)pl.items.size(), pl.p2p_src.get(),
                op.max_item_sources, w, op.part.get(), sn, pl.p2p_order.get(), &op.p2p_aux,
-               op.p2p_sched.get(), op.srec.get());
+               op.p2p_sched.get(), op.srec.get(), op.s_panel.get(), c.x);
   record(op, ST_P2P, true, sn);
   if (!serial) FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
   // far field on the main stream

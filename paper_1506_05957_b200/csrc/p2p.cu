@@ -255,7 +255,8 @@ template <int NCT, int NSTG>
 __global__ void __launch_bounds__(NCT + LAPD_PROD, 1)
 k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4* __restrict__ gl_ltab,
            const int* __restrict__ gl_slot, const int* __restrict__ gl_spec, int max_src, int max_leaves, int max_tgt,
-           const double2* __restrict__ srec, double* __restrict__ part, unsigned* __restrict__ sched,
+           const double2* __restrict__ srec, const int* __restrict__ s_panel, const double* __restrict__ xd,
+           double* __restrict__ part, unsigned* __restrict__ sched,
            long long* __restrict__ trace) {
   constexpr int TPT = LAPD_TPT, NPT = LAPD_PROD, ALL = NCT + NPT;
   // optional per-item clock trace (FMMBEM_P2P_TRACE): [cta][item < 32][8]
@@ -318,6 +319,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
       // flattened over the tile: 4 sources per thread per round, loads issued before use
       for (int i0 = pt; i0 < H.ns; i0 += 4 * NPT) {
         double2 v[4][3];
+        int pn[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int i = min(i0 + u * NPT, H.ns - 1);
@@ -328,11 +330,16 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
             else hi = mid - 1;
           }
           const int4 e = ltab[lo];
-          const size_t g = (size_t)(e.x + i - e.z) * 3;
+          const int gi = e.x + i - e.z;
+          const size_t g = (size_t)gi * 3;
           v[u][0] = srec[g];
           v[u][1] = srec[g + 1];
           v[u][2] = srec[g + 2];
+          pn[u] = s_panel[gi];
         }
+        double xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = xd[pn[u]];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int i = i0 + u * NPT;
@@ -346,7 +353,8 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
           }
           const int dst = (r < H.nspec && spec[r] == i) ? r : H.nspec + i - r;
           const double sx = v[u][0].x - H.cx, sy = v[u][0].y - H.cy, sz = v[u][1].x - H.cz;
-          const double dx = v[u][1].y, dy = v[u][2].x, dz = v[u][2].y;
+          // dipole d = (w n) x[panel] (bemop.py:188-203, 213-216)
+          const double dx = v[u][1].y * xv[u], dy = v[u][2].x * xv[u], dz = v[u][2].y * xv[u];
           const double ss = fma(sx, sx, fma(sy, sy, sz * sz));
           const double ds = fma(dx, sx, fma(dy, sy, dz * sz));
           sh2[dst] = make_double2(-2.0 * sx, -2.0 * sy);
@@ -453,6 +461,13 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
 
 long long* p2p_trace_buffer();
 
+bool p2p_lapd_usable(const P2PAux* aux, int max_sources) {
+  const int ms = std::max(max_sources, 1);
+  return aux && aux->ready && aux->max_tgt <= LAPD_CONS * LAPD_TPT &&
+         2 * (LapdStage(ms, aux->max_leaves, aux->max_tgt).bytes + (size_t)384 * LAPD_TPT * sizeof(double)) <=
+             227 * 1024;
+}
+
 void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& items,
                    const std::vector<int>& p2p_src, const std::vector<int>& self_src_sorted,
                    cudaStream_t st) {
@@ -522,8 +537,8 @@ long long* p2p_trace_buffer() {
   return buf;
 }
 
-void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const double2* srec, double* part,
-                     cudaStream_t st, unsigned* sched) {
+void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const double2* srec,
+                     const int* s_panel, const double* x, double* part, cudaStream_t st, unsigned* sched) {
   const LapdStage L(max_src, aux.max_leaves, aux.max_tgt);
   static const int nct = std::getenv("FMMBEM_P2P_NCT") ? std::atoi(std::getenv("FMMBEM_P2P_NCT")) : LAPD_CONS;
   const size_t per = L.bytes + (size_t)nct * LAPD_TPT * sizeof(double);
@@ -543,7 +558,8 @@ void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const dou
   if (grid > 0)
     kern<<<grid, nthr, smem, st>>>(T, aux.hdr.get(), aux.n_items, aux.ltab.get(), aux.slot.get(),
                                    aux.spec.get(), max_src,
-                                   aux.max_leaves, aux.max_tgt, srec, part, sched, p2p_trace_buffer());
+                                   aux.max_leaves, aux.max_tgt, srec, s_panel, x, part, sched,
+                                   p2p_trace_buffer());
   FMM_LAUNCH_CHECK();
 }
 
@@ -565,16 +581,13 @@ void launch_p2p_t(const TreeDev& S, const TreeDev& T, const P2PItem* items, int 
 void launch_p2p(P2PKind kind, const TreeDev& S, const TreeDev& T, const P2PItem* items,
                 int n_items, const int* p2p_src, int max_sources, const double* w, double* part,
                 cudaStream_t st, const int* order, const P2PAux* aux, unsigned* sched,
-                const double2* srec) {
+                const double2* srec, const int* s_panel, const double* x) {
   const int ms = std::max(max_sources, 1);
   switch (kind) {
     case P2PKind::LAP_Q: return launch_p2p_t<P2PKind::LAP_Q>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
     case P2PKind::LAP_D:
-      if (aux && aux->ready && sched && srec &&
-          aux->max_tgt <= LAPD_CONS * LAPD_TPT &&
-          2 * (LapdStage(ms, aux->max_leaves, aux->max_tgt).bytes +
-               (size_t)384 * LAPD_TPT * sizeof(double)) <= 227 * 1024)
-        return launch_p2p_lapd(T, *aux, ms, srec, part, st, sched);
+      if (p2p_lapd_usable(aux, ms) && sched && srec && s_panel && x)
+        return launch_p2p_lapd(T, *aux, ms, srec, s_panel, x, part, st, sched);
       return launch_p2p_t<P2PKind::LAP_D>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
     case P2PKind::STOKESLET: return launch_p2p_t<P2PKind::STOKESLET>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
     case P2PKind::STRESSLET: return launch_p2p_t<P2PKind::STRESSLET>(S, T, items, n_items, p2p_src, ms, w, part, st, order);
