@@ -144,7 +144,7 @@ struct EpiArgs {
 // L2P columns m = k mod NS, every NS-th near-field item and correction entry;
 // the slices' partials are added in slice order.
 template <int KIND> constexpr int epi_slices() { return EpiTraits<KIND>::C == 1 ? 4 : 1; }
-constexpr int EPI_TGT = 128;  // targets per pass
+constexpr int EPI_TGT = 128;  // targets per CTA (blockIdx.y: the leaf's target tile)
 
 template <int KIND, bool FAR>
 __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeDev T, EpiArgs a) {
@@ -159,12 +159,14 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
   const int t0 = T.body_start[leaf], nt = T.body_count[leaf];
   const int ib = a.item_begin[li], ie = a.item_begin[li + 1];
   const int tl = threadIdx.x % EPI_TGT, slice = threadIdx.x / EPI_TGT;
+  if ((int)blockIdx.y * EPI_TGT >= nt) return;  // (uniform over the CTA, before any barrier)
   // every path cell's local expansion (the leaf, then its ancestors with M2L terms), staged once
   for (int i = threadIdx.x; i < np * C * H; i += blockDim.x) {
     const int k = i / (C * H), r = i - k * (C * H);
     sL[i] = a.L[(size_t)a.path[pb + k] * C * H + r];
   }
-  for (int base = 0; base < nt; base += EPI_TGT) {
+  {
+    const int base = blockIdx.y * EPI_TGT;
     const int lt = base + tl;
     const bool valid = lt < nt;
     const int ti = t0 + (valid ? lt : 0);
@@ -272,14 +274,15 @@ void launch_epilogue(BemOp& op, const EpiArgs& a, bool far, cudaStream_t s, int 
   const size_t lbytes = (size_t)std::max(a.max_path, 1) * C * sizeof(double2);
   const size_t smem = (far ? lbytes * hcount(a.p) : 0) + red;
   if (nl <= 0) return;
+  const int tiles = (std::max(op.plan.tgt.max_leaf_count, 1) + EPI_TGT - 1) / EPI_TGT;
   if (far) {
     const size_t most = lbytes * hcount(P_MAX) + red;
     FMM_REQUIRE(smem <= 227 * 1024, "epilogue: root paths too long for shared memory");
     FMM_CUDA(cudaFuncSetAttribute(k_epilogue<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)std::min<size_t>(most, 227 * 1024)));
-    k_epilogue<KIND, true><<<nl, EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
+    k_epilogue<KIND, true><<<dim3(nl, tiles), EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
   } else {
-    k_epilogue<KIND, false><<<nl, EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
+    k_epilogue<KIND, false><<<dim3(nl, tiles), EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
   }
   FMM_LAUNCH_CHECK();
 }

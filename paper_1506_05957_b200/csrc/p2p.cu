@@ -212,6 +212,12 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct LapdStage {  // shared-memory stage layout (offsets in bytes from the stage base)
   size_t planes, tgt, ltab, slot, spec, bytes;
   __host__ __device__ LapdStage(int max_src, int max_leaves, int max_tgt) {
@@ -261,7 +267,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
   constexpr int TPT = LAPD_TPT, NPT = LAPD_PROD, ALL = NCT + NPT;
   // optional per-item clock trace (FMMBEM_P2P_TRACE): [cta][item < 32][8]
 #define TR(k, j)                                                              \
-  if (trace && (k) < 32) trace[((size_t)blockIdx.x * 32 + (k)) * 8 + (j)] = clock64()
+  if (trace && (k) < 32) trace[((size_t)blockIdx.x * 32 + (k)) * 8 + (j)] = (long long)globaltimer_ns()
   extern __shared__ __align__(16) unsigned char smem[];
   const LapdStage L(max_src, max_leaves, max_tgt);
   double* red = reinterpret_cast<double*>(smem + NSTG * L.bytes);  // [NSTG][NCT * TPT] group partials

@@ -1,7 +1,7 @@
 """Per-item clock trace of the persistent double-layer P2P kernel (FMMBEM_P2P_TRACE=1).
 
 python tools/p2p_trace.py cfg2 12
-Per CTA and item: producer (wait EMPTY, stage) and consumer (wait FULL, loop warp 0 / last warp,
+Per CTA and item (globaltimer ns): producer (wait EMPTY, stage) and consumer (wait FULL, loop warp 0 / last warp,
 reduce) phases in cycles; summarised over CTAs.
 """
 import ctypes
@@ -47,5 +47,12 @@ for c in ctas:
         prev_end = t[c, k, 7]
 n = max(len(ctas), 1)
 print(name, p, "ctas", len(ctas), {k: round(v / n) for k, v in tot.items()})
+# globaltimer (ns): kernel-wide view
+starts = np.array([t[c, 0, 0] for c in ctas])
+ends = np.array([max(t[c, k, 7] for k in range(32) if t[c, k, 7] != 0) for c in ctas])
+first_full = np.array([t[c, 0, 2] for c in ctas])
+t0 = starts.min()
+print("ns: cta start spread", int(starts.max() - t0), "first item staged (median)", int(np.median(first_full - t0)),
+      "cta end min/median/max", int(ends.min() - t0), int(np.median(ends - t0)), int(ends.max() - t0))
 last = sorted(((c, [int(t[c, k, 2] - t[c, k, 1]) for k in range(32) if t[c, k, 2]]) for c in ctas[:1]))
 print("producer stage cycles per item (cta 0):", last)
