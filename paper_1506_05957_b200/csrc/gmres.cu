@@ -177,6 +177,62 @@ __global__ void __launch_bounds__(RT) k_arnoldi(int64_t n, int k, const double* 
   for (int64_t i = i0; i < n; i += stride) w[i] = xnext[i] = h > 0.0 ? w[i] / h : 0.0;
 }
 
+// The grid-wide step with w held in registers (GE elements per thread) and the next basis
+// vector prefetched before each grid barrier: a sweep reads v_j once instead of reading v_j
+// and reading + writing w (n up to AB * GT * GE).
+constexpr int GT = 512;  // threads per CTA
+
+template <int GE>
+__global__ void __launch_bounds__(GT) k_arnoldi_reg(int64_t n, int k, const double* __restrict__ V,
+                                                    const double* __restrict__ w0, double* w,
+                                                    double* xnext, double* partials, double* hd,
+                                                    double* mbox, unsigned long long* mflag,
+                                                    unsigned long long seq) {
+  __shared__ double sh[GT / 32];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double wr[GE], vc[GE], vn[GE];
+#pragma unroll
+  for (int e = 0; e < GE; ++e) {
+    const int64_t i = i0 + e * stride;
+    wr[e] = i < n ? w0[i] : 0.0;
+    vn[e] = i < n ? V[i] : 0.0;
+  }
+  double h = 0.0;
+  for (int j = 0; j <= k + 1; ++j) {
+    double acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < GE; ++e) {
+      if (j) wr[e] = fma(-h, vc[e], wr[e]);  // w -= h_{j-1} v_{j-1}
+      vc[e] = vn[e];
+    }
+    if (j + 1 <= k) {
+#pragma unroll
+      for (int e = 0; e < GE; ++e) {
+        const int64_t i = i0 + e * stride;
+        vn[e] = i < n ? V[(size_t)(j + 1) * n + i] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < GE; ++e) acc = j <= k ? fma(vc[e], wr[e], acc) : fma(wr[e], wr[e], acc);
+    h = grid_total(block_sum(acc, sh), partials + (j & 1) * gridDim.x, sh);
+    if (j > k) h = sqrt(h);
+    if (i0 == 0) {
+      hd[j] = h;
+      mbox[j] = h;
+    }
+  }
+  if (i0 == 0) {  // the column is complete: post it to the host
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(mflag) = seq;
+  }
+#pragma unroll
+  for (int e = 0; e < GE; ++e) {
+    const int64_t i = i0 + e * stride;
+    if (i < n) w[i] = xnext[i] = h > 0.0 ? wr[e] / h : 0.0;
+  }
+}
+
 // The same Arnoldi step for n <= ACL * ACT * AE on one thread-block cluster: w stays in
 // registers (AE elements per thread), each sweep's CTA partials are exchanged through
 // distributed shared memory and added in rank order by every CTA (bitwise-identical h_j),
@@ -407,7 +463,15 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
         FMM_CUDA(cudaLaunchKernelEx(&cfg, k_arnoldi_cluster, (int)n, kk, Vc, w0, w, xn, hd, mb, mf, sq));
       } else {
         void* args[] = {&nn, &kk, &Vc, &w0, &w, &xn, &pp, &hd, &mb, &mf, &sq};
-        FMM_CUDA(cudaLaunchCooperativeKernel((const void*)k_arnoldi, dim3(AB), dim3(RT), args, 0, s));
+        const int64_t cap = (int64_t)AB * GT;
+        const void* kern = n <= cap ? (const void*)k_arnoldi_reg<1>
+                         : n <= 2 * cap ? (const void*)k_arnoldi_reg<2>
+                         : n <= 4 * cap ? (const void*)k_arnoldi_reg<4>
+                         : n <= 8 * cap ? (const void*)k_arnoldi_reg<8> : nullptr;
+        if (kern)
+          FMM_CUDA(cudaLaunchCooperativeKernel(kern, dim3(AB), dim3(GT), args, 0, s));
+        else
+          FMM_CUDA(cudaLaunchCooperativeKernel((const void*)k_arnoldi, dim3(AB), dim3(RT), args, 0, s));
       }
     }
     FMM_LAUNCH_CHECK();

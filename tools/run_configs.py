@@ -40,11 +40,17 @@ def run(name):
     for relaxed in ((True, False) if name == "cfg2" else (True,)):
         solve(op, b, eta=cfg.tol, p_initial=cfg.p_initial, p_min=cfg.p_min, relaxed=relaxed,
               max_iter=cfg.max_iter)  # warm: graphs per p
-        op.set_timing(True)
-        op.stage_times(reset=True)
+        # time to solution: the plain graphs (CUDA events around the device GMRES call)
         res = solve(op, b, eta=cfg.tol, p_initial=cfg.p_initial, p_min=cfg.p_min, relaxed=relaxed,
                     max_iter=cfg.max_iter)
         ms = op.counters()[2]
+        # per-stage times from a separate instrumented solve
+        op.set_timing(True)
+        solve(op, b, eta=cfg.tol, p_initial=cfg.p_initial, p_min=cfg.p_min, relaxed=relaxed,
+              max_iter=cfg.max_iter)  # (captures the instrumented graphs)
+        op.stage_times(reset=True)
+        solve(op, b, eta=cfg.tol, p_initial=cfg.p_initial, p_min=cfg.p_min, relaxed=relaxed,
+              max_iter=cfg.max_iter)
         st, calls = op.stage_times(reset=True)
         op.set_timing(False)
         tag = "relaxed" if relaxed else "fixed"
