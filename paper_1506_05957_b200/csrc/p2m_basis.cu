@@ -120,7 +120,7 @@ k_p2m_basis(const int* __restrict__ leaves, const int* __restrict__ body_start,
 // 4 warps split the item's (<= 32) entries, lanes run over h (NJ = ceil(H/32)
 // per lane, every row load a coalesced 512 B), the warps' sums are added in
 // warp order through shared memory.
-constexpr int P2M_CHUNK = 32;
+constexpr int P2M_CHUNK = 64;
 
 template <int NJ>
 __global__ void __launch_bounds__(128)
@@ -138,20 +138,30 @@ k_p2m_basis_cl(const int4* __restrict__ items, const int* __restrict__ red_of,
   double2 acc[NJ];
 #pragma unroll
   for (int j = 0; j < NJ; ++j) acc[j] = make_double2(0.0, 0.0);
+  // batches of P2M_BATCH rows: all their loads are issued before the first use
+  // (memory-level parallelism: the stream is latency-bound otherwise)
+  constexpr int P2M_BATCH = 4;
 #pragma unroll
-  for (int k = 0; k < P2M_CHUNK / 4; ++k) {
-    const int e = warp + 4 * k;
-    if (e < len) {
-      const double s = sx[e];
-      const double2* row = B + (size_t)(it.y + e) * Hp;
+  for (int k0 = 0; k0 < P2M_CHUNK / 4; k0 += P2M_BATCH) {
+    double2 v[P2M_BATCH][NJ];
+#pragma unroll
+    for (int u = 0; u < P2M_BATCH; ++u) {
+      const int e = warp + 4 * (k0 + u);
+      const double2* row = B + (size_t)(it.y + min(e, len - 1)) * Hp;
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         const int h = lane + 32 * j;
-        if (h < H) {
-          const double2 v = __ldg(row + h);
-          acc[j].x = fma(s, v.x, acc[j].x);
-          acc[j].y = fma(s, v.y, acc[j].y);
-        }
+        v[u][j] = (e < len && h < H) ? __ldg(row + h) : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < P2M_BATCH; ++u) {
+      const int e = warp + 4 * (k0 + u);
+      const double s = e < len ? sx[e] : 0.0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        acc[j].x = fma(s, v[u][j].x, acc[j].x);
+        acc[j].y = fma(s, v[u][j].y, acc[j].y);
       }
     }
   }
