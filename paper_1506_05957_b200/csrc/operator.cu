@@ -61,6 +61,11 @@ __global__ void k_source_records(int64_t ns, const double* px, const double* py,
   srec[3 * i + 2] = make_double2(w * nrm[3 * pn + 1], w * nrm[3 * pn + 2]);
 }
 
+__global__ void k_row_ranges(int64_t n, const int* perm, const int* rowptr, int2* rows) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) rows[i] = make_int2(rowptr[perm[i]], rowptr[perm[i] + 1]);
+}
+
 __global__ void k_invert_perm(int64_t n, const int* perm, int* inv) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) inv[perm[i]] = (int)i;
@@ -131,6 +136,7 @@ struct EpiArgs {
   int max_path;
   int p;
   const int* rowptr;
+  const int2* rows;  // per sorted target: [start, end) of its correction row (no perm lookup)
   const int* cols;
   const double* vals;
   const double* x;
@@ -175,17 +181,19 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
     double near[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) near[c] = 0.0;
+    // a leaf's items are consecutive with out_off advancing by nt (plan_make_items)
+    const int oo = ib < ie ? a.items[ib].out_off : 0;
     if (valid)
       for (int it = ib + slice; it < ie; it += NS) {
-        const double* pp = a.part + (size_t)(a.items[it].out_off + lt) * NC;
+        const double* pp = a.part + (size_t)(oo + (it - ib) * nt + lt) * NC;
 #pragma unroll
         for (int c = 0; c < NC; ++c) near[c] += pp[c];
       }
     double corr1 = 0.0;
     if ((KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) && valid) {
-      const int e1 = a.rowptr[pn + 1];
+      const int2 rr = a.rows[ti];
 #pragma unroll 4
-      for (int e = a.rowptr[pn] + slice; e < e1; e += NS) corr1 = fma(a.vals[e], a.x[a.cols[e]], corr1);
+      for (int e = rr.x + slice; e < rr.y; e += NS) corr1 = fma(a.vals[e], a.x[a.cols[e]], corr1);
     }
     double pot[C], grad[3 * C];
 #pragma unroll
@@ -432,6 +440,9 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
     op.max_item_sources = std::max(op.max_item_sources, acc);
   }
   build_near_pairs(op, s);
+  op.near_rows.resize(P);
+  k_row_ranges<<<grid_for(P, 256), 256, 0, s>>>(P, op.plan.tgt.perm.get(), op.near_rowptr.get(), op.near_rows.get());
+  FMM_LAUNCH_CHECK();
   int sys_kind, rhs_kind;
   if (formulation == LAPLACE_FIRST) { sys_kind = K_LAP_SINGLE; rhs_kind = K_LAP_DOUBLE; }
   else if (formulation == LAPLACE_SECOND) { sys_kind = K_LAP_DOUBLE; rhs_kind = K_LAP_SINGLE; }
@@ -537,6 +548,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   a.max_path = pl.max_path;
   a.p = c.p;
   a.rowptr = op.near_rowptr.get();
+  a.rows = op.near_rows.get();
   a.cols = op.near_cols.get();
   a.vals = c.corr->vals.get();
   a.x = c.x;

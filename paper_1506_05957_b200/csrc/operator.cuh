@@ -87,6 +87,7 @@ struct BemOp {
   // near pairs (CSR by target panel) and the two corrections
   int near_nnz = 0;
   DevBuf<int> near_rowptr, near_cols;
+  DevBuf<int2> near_rows;  // per sorted target: its correction row range
   Correction c_sys, c_rhs;
 
   // work buffers
