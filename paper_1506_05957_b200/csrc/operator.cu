@@ -166,10 +166,18 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
   const int ib = a.item_begin[li], ie = a.item_begin[li + 1];
   const int tl = threadIdx.x % EPI_TGT, slice = threadIdx.x / EPI_TGT;
   if ((int)blockIdx.y * EPI_TGT >= nt) return;  // (uniform over the CTA, before any barrier)
-  // every path cell's local expansion (the leaf, then its ancestors with M2L terms), staged once
+  // every path cell's local expansion (the leaf, then its ancestors with M2L terms) and its
+  // centre, staged once (the L2P loop below then touches no global memory)
+  __shared__ double s_cc[3 * 24];
   for (int i = threadIdx.x; i < np * C * H; i += blockDim.x) {
     const int k = i / (C * H), r = i - k * (C * H);
     sL[i] = a.L[(size_t)a.path[pb + k] * C * H + r];
+  }
+  if (FAR && threadIdx.x < np) {
+    const int cell = a.path[pb + threadIdx.x];
+    s_cc[3 * threadIdx.x] = T.cx[cell];
+    s_cc[3 * threadIdx.x + 1] = T.cy[cell];
+    s_cc[3 * threadIdx.x + 2] = T.cz[cell];
   }
   {
     const int base = blockIdx.y * EPI_TGT;
@@ -177,6 +185,7 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
     const bool valid = lt < nt;
     const int ti = t0 + (valid ? lt : 0);
     const int pn = T.perm[ti];
+    const double tx = T.px[ti], ty = T.py[ti], tz = T.pz[ti];
     // near-field partials and the correction row first: their loads overlap the L2P below
     double near[NC];
 #pragma unroll
@@ -202,14 +211,11 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
       __syncthreads();  // (first pass: the staged expansions)
       if (valid)
         for (int k = 0; k < np; ++k) {
-          const int cell = a.path[pb + k];
+          const double dx = tx - s_cc[3 * k], dy = ty - s_cc[3 * k + 1], dz = tz - s_cc[3 * k + 2];
           if (C == 1)
-            pot[0] += l2p_eval1(sL + (size_t)k * H, a.p, T.px[ti] - T.cx[cell], T.py[ti] - T.cy[cell],
-                                T.pz[ti] - T.cz[cell], slice);
+            pot[0] += l2p_eval1(sL + (size_t)k * H, a.p, dx, dy, dz, slice);
           else
-            l2p_eval<C, Tr::GRAD>(sL + (size_t)k * C * H, H, a.p, T.px[ti] - T.cx[cell],
-                                  T.py[ti] - T.cy[cell], T.pz[ti] - T.cz[cell], pot, grad, T.rec,
-                                  slice, NS);
+            l2p_eval<C, Tr::GRAD>(sL + (size_t)k * C * H, H, a.p, dx, dy, dz, pot, grad, T.rec, slice, NS);
         }
     }
     if (KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) {
@@ -233,7 +239,6 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
         else a.y[pn] = v;
       }
     } else if (valid) {
-      const double tx = T.px[ti], ty = T.py[ti], tz = T.pz[ti];
       const double xt[3] = {tx, ty, tz};
       double u[3];
       for (int i = 0; i < 3; ++i) {
