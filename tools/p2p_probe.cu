@@ -30,7 +30,10 @@ __global__ void lapd_loop(const double2* __restrict__ src, int reps, double* out
     acc[q] = 0.0;
     self[q] = (threadIdx.x * 7 + q) % NSRC;
   }
-  const int G = MODE == 4 ? Grt : 8, g = threadIdx.x % G;  // lanes of a warp read 8 distinct sources
+  // MODE 5: the production mapping, nsl = Grt target slots, G = 256 / nsl groups, g = tid / nsl
+  const int G = MODE == 4 ? Grt : MODE == 5 ? (int)blockDim.x / Grt : 8;
+  const int g = MODE == 5 ? (int)threadIdx.x / Grt : (int)threadIdx.x % G;
+  if (g >= G) return;
   const int nsl = MODE == 4 ? nsrt : NSRC;
   for (int r = 0; r < reps; ++r) {
     for (int j = g; j < nsl; j += G) {
@@ -42,7 +45,14 @@ __global__ void lapd_loop(const double2* __restrict__ src, int reps, double* out
           d2 = __hiloint2double(j == self[q] ? 0x7E37E43C : __double2hiint(d2), __double2loint(d2));
         double y;
         if (MODE == 2) y = (double)rsqrtf((float)d2);
-        else asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
+        else if (MODE == 6) {
+          // fp32 seed on the XU: d2 -> float by bit surgery (integer pipe), MUFU.RSQ, back
+          const int fb = __funnelshift_l(__double2loint(d2), __double2hiint(d2), 3) - (896 << 23);
+          float yf;
+          asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(__int_as_float(fb)));
+          const int yb = __float_as_int(yf);
+          y = __hiloint2double((yb >> 3) + (896 << 20), yb << 29);
+        } else asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
         const double y2 = y * y;
         const double y3 = y2 * y;
         const double e = fma(-d2, y2, 1.0);
@@ -78,20 +88,21 @@ __global__ void mufu_lat(double* out, int n) {
 }
 
 __global__ void mufu_tput(double* out, int n) {
-  double x0 = 1.0 + threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
-  double a = 0;
+  // 8 independent chains y <- rsqrt(y + 1) (one DADD per MUFU, so the DP pipe is not the limit)
+  double x[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) x[q] = 1.0 + threadIdx.x + q;
   for (int i = 0; i < n; ++i) {
-    double y0, y1, y2, y3, y4, y5, y6, y7;
-    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(x0));
-    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y1) : "d"(x1));
-    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y2) : "d"(x2));
-    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y3) : "d"(x3));
-    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y4) : "d"(x4));
-    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y5) : "d"(x5));
-    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y6) : "d"(x6));
-    asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y7) : "d"(x7));
-    a += y0 + y1 + y2 + y3 + y4 + y5 + y6 + y7;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      double y;
+      asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x[q]));
+      x[q] = y + 1.0;
+    }
   }
+  double a = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a += x[q];
   if (a == 1.2345) out[0] = a;
 }
 
@@ -158,10 +169,31 @@ int main() {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double n = 8.0 * 2048 * sms * 4 * 256;
-    printf("{\"rsq64h_per_clk_per_sm\": %.2f}\n", n / (ms * 1e-3) / (sms * clk * 1e9));
+    printf("{\"rsq64h_per_clk_per_sm\": %.2f, \"ms\": %.3f}\n", n / (ms * 1e-3) / (sms * clk * 1e9), ms);
   }
   for (int c : {1, 3}) run<4, 0>(src, out, sms, 256, c, clk);
   for (int c : {1, 3}) run<4, 1>(src, out, sms, 256, c, clk);
   for (int c : {1, 3}) run<4, 4>(src, out, sms, 256, c, clk);
+  for (int c : {1, 3}) run<4, 6>(src, out, sms, 256, c, clk);
+  for (int nsl : {19, 32, 64}) {
+    printf("nsl %d: ", nsl);
+    // (run<> prints one line)
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = sms * 1, reps = 16;
+    lapd_loop<4, 5><<<blocks, 256>>>(src, 1, out, nsl, NSRC);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    lapd_loop<4, 5><<<blocks, 256>>>(src, reps, out, nsl, NSRC);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const int G = 256 / nsl;
+    const double inter = (double)blocks * G * nsl * 4 * ((NSRC + G - 1) / G) * reps;
+    printf("{\"mode\": 5, \"nsl\": %d, \"dp_pipe_frac_active_threads\": %.3f}\n", nsl,
+           inter * 13.0 / (ms * 1e-3) / (sms * 64.0 * clk * 1e9));
+  }
   return 0;
 }
