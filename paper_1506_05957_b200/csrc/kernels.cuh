@@ -34,7 +34,8 @@ void launch_m2m(const Tree& S, const std::vector<int>& level_off, const int* cel
 // (gitems, cells: optional restricted work lists for a shard; defaults = whole plan)
 void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
                 cudaStream_t st, const int4* gitems = nullptr, int n_gitems = -1,
-                const int* cells = nullptr, int n_cells = -1, const int* gpair = nullptr);
+                const int* cells = nullptr, int n_cells = -1, const int* gpair = nullptr,
+                const int4* citems = nullptr, int n_citems = -1, const int* cpair = nullptr);
 void compute_igrid_full(const double* d_off, int n_off, int order, double2* out, cudaStream_t s);
 void compute_rot_tables(const double* d_off, int n_off, int P, double* out, double* geo,
                         cudaStream_t s);
@@ -44,7 +45,7 @@ inline size_t rot_aux_size(int P) { return (size_t)(4 * P + 4); }
 void build_rot_aux(const double* geo, int n_off, int P, double* aux, cudaStream_t s);
 void build_rot_frag(const double* rot, int n_off, int P, double* out, cudaStream_t s);
 void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
-                    int C, const double2* M, double2* pout, cudaStream_t st);
+                    int C, const double2* M, double2* pout, cudaStream_t st, bool cls);
 constexpr int M2L_ROT_MIN_P = 3;  // rotation-based M2L from this order up
 // M2M through octant-grouped child translations (cout: per-cell child contributions)
 void launch_m2m_grouped(const Plan& plan, int p, int C, const double2* rfull, double2* M,

@@ -189,10 +189,13 @@ __global__ void k_rot_aux(const double* __restrict__ geo, int n_off, int P, doub
 // warp unit = (item, octet of vectors); vector v of an item = (pair v / C, channel v % C).
 // Everything is unrolled for the compile-time order P; the next degree's operator
 // fragments are loaded while the current degree multiplies.
-template <int P>
+// CLS: the item's vectors may come from different offsets of one class (same polar-angle
+// tables and |D|): the azimuthal phases are read per vector into registers; otherwise the
+// item shares one offset and its phases are read once into shared memory.
+template <int P, bool CLS>
 __global__ void __launch_bounds__(ROT_WARPS * 32)
 k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ gpair,
-          const int* __restrict__ pair_src, const double* __restrict__ frag,
+          const int* __restrict__ pair_src, const int* __restrict__ pair_off, const double* __restrict__ frag,
           const int* __restrict__ dir, int ttot,
           const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
           double2* __restrict__ pout) {
@@ -238,9 +241,24 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
   // (k = 4t + fc, vector fr) comes straight from global memory, so the degrees are
   // independent and need no synchronisation; next degree's operands are in flight
   const double2* msrc = nullptr;
+  // azimuthal phases e^{-ik phi} of each vector's own offset (the item's pairs share the
+  // polar-angle tables and |D|, not necessarily phi): stage A's column fr, outputs 2fc, 2fc+1
+  const int astr = aux_stride(aux_p);
+  double2 phA[CLS ? FRAG_KS_MAX : 1];  // (CLS) e^{-ik phi} of column fr's offset at k = 4t + fc
   {
     const int vg = v0 + fr;
-    if (vg < nvec) msrc = M + ((size_t)pair_src[gpair[it.y + vg / C]] * C + vg % C) * H;
+    int uo = u;
+    if (vg < nvec) {
+      const int pr = gpair[it.y + vg / C];
+      msrc = M + ((size_t)pair_src[pr] * C + vg % C) * H;
+      uo = pair_off[pr];
+    }
+    if constexpr (CLS) {
+      const double2* pa = reinterpret_cast<const double2*>(aux + (size_t)uo * astr);
+#pragma unroll
+      for (int t = 0; t < FRAG_KS_MAX; ++t)
+        phA[t] = 4 * t + fc <= P ? __ldg(pa + 4 * t + fc) : make_double2(0.0, 0.0);
+    }
   }
   __syncwarp();  // ph, zz
   struct BIn {
@@ -264,7 +282,7 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
     for (int t = 0; t < FRAG_KS_MAX; ++t)
       if (t < ks) {
         const int col = t * 4 + fc;
-        const double2 x = col <= n ? cmul(ph[col], b.m[t]) : make_double2(0.0, 0.0);
+        const double2 x = col <= n ? cmul(CLS ? phA[CLS ? t : 0] : ph[col], b.m[t]) : make_double2(0.0, 0.0);
 #pragma unroll
         for (int q = 0; q < 3; ++q)
           if (q < mt) {
@@ -375,10 +393,17 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
   };
   // stage C and the output phase; lane owns vectors v0 + 2 fc and v0 + 2 fc + 1
   double2* dst[2];
+  double2 phO[2][CLS ? 3 : 1];  // (CLS) e^{-ik phi} of output vector 2 fc + w at k = 8 q + fr
 #pragma unroll
   for (int w = 0; w < 2; ++w) {
     const int vg = v0 + 2 * fc + w;
-    dst[w] = vg < nvec ? pout + ((size_t)gpair[it.y + vg / C] * C + vg % C) * H : nullptr;
+    const int pr = vg < nvec ? gpair[it.y + vg / C] : 0;
+    dst[w] = vg < nvec ? pout + ((size_t)pr * C + vg % C) * H : nullptr;
+    if constexpr (CLS) {
+      const double2* po = reinterpret_cast<const double2*>(aux + (size_t)(vg < nvec ? pair_off[pr] : u) * astr);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) phO[w][q] = 8 * q + fr <= P ? __ldg(po + 8 * q + fr) : make_double2(0.0, 0.0);
+    }
   }
 #pragma unroll
   for (int j = 0; j <= P; ++j) {
@@ -390,9 +415,9 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
     for (int q = 0; q < 3; ++q) {
       const int k = q * 8 + fr;
       if (q < frag_mt(j) && k <= j) {
-        const double2 e = ph[k];
-        if (dst[0]) dst[0][hb + k] = cmul(e, make_double2(ar[q].x, ai[q].x));
-        if (dst[1]) dst[1][hb + k] = cmul(e, make_double2(ar[q].y, ai[q].y));
+        const double2 e0 = CLS ? phO[0][CLS ? q : 0] : ph[k], e1 = CLS ? phO[1][CLS ? q : 0] : ph[k];
+        if (dst[0]) dst[0][hb + k] = cmul(e0, make_double2(ar[q].x, ai[q].x));
+        if (dst[1]) dst[1][hb + k] = cmul(e1, make_double2(ar[q].y, ai[q].y));
       }
     }
     if (j < P) cur = nxt;
@@ -401,17 +426,19 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
 
 template <int P>
 void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int C,
-                  const double2* M, double2* pout, cudaStream_t st) {
+                  const double2* M, double2* pout, cudaStream_t st, bool cls) {
   constexpr int H = hcount(P);
   const size_t smem = (size_t)ROT_WARPS * (16 * H + 4 * P + 4) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   const int64_t units = (int64_t)n_items * C;
-  k_m2l_rot<P><<<(unsigned)((units + ROT_WARPS - 1) / ROT_WARPS), ROT_WARPS * 32, smem, st>>>(
-      gitems, n_items, gpair, plan.m2l_src.get(), plan.rotf.get(), plan.rot_dir.get(),
+  auto kern = cls ? k_m2l_rot<P, true> : k_m2l_rot<P, false>;
+  kern<<<(unsigned)((units + ROT_WARPS - 1) / ROT_WARPS), ROT_WARPS * 32, smem, st>>>(
+      gitems, n_items, gpair, plan.m2l_src.get(), plan.m2l_off.get(), plan.rotf.get(), plan.rot_dir.get(),
       frag_base(plan.rot_p + 1),
       plan.rot_aux.get(), plan.rot_p, M, C, pout);
   FMM_LAUNCH_CHECK();
@@ -420,10 +447,10 @@ void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_
 template <int... Ps>
 void launch_rot_dispatch(std::integer_sequence<int, Ps...>, int p, const Plan& plan,
                          const int4* gitems, const int* gpair, int n_items, int C,
-                         const double2* M, double2* pout, cudaStream_t st) {
+                         const double2* M, double2* pout, cudaStream_t st, bool cls) {
   bool done = false;
   ((p == Ps + M2L_ROT_MIN_P && !done
-        ? (launch_rot_p<Ps + M2L_ROT_MIN_P>(plan, gitems, gpair, n_items, C, M, pout, st), done = true)
+        ? (launch_rot_p<Ps + M2L_ROT_MIN_P>(plan, gitems, gpair, n_items, C, M, pout, st, cls), done = true)
         : false),
    ...);
   FMM_REQUIRE(done, "rotation M2L order out of range");
@@ -457,11 +484,11 @@ void build_rot_aux(const double* geo, int n_off, int P, double* aux, cudaStream_
 }
 
 void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
-                    int C, const double2* M, double2* pout, cudaStream_t st) {
+                    int C, const double2* M, double2* pout, cudaStream_t st, bool cls) {
   if (n_items <= 0) return;
   FMM_REQUIRE(p <= plan.rot_p, "rotation tables not prepared for this order");
   launch_rot_dispatch(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, plan, gitems,
-                      gpair, n_items, C, M, pout, st);
+                      gpair, n_items, C, M, pout, st, cls);
 }
 
 }  // namespace fmmbem

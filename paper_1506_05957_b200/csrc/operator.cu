@@ -531,7 +531,8 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     record(op, ST_M2L, false, s);
     if (sharded)
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s, sw.gitems.get(),
-                 (int)sw.gitems_h.size(), sw.gather_cells.get(), sw.n_gather_cells, sw.gpair.get());
+                 (int)sw.gitems_h.size(), sw.gather_cells.get(), sw.n_gather_cells, sw.gpair.get(),
+                 sw.citems.get(), sw.n_citems, sw.cpair.get());
     else
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);

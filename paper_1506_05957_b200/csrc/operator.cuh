@@ -41,6 +41,9 @@ struct ShardWork {
   std::vector<int4> gitems_h;
   DevBuf<int4> gitems;
   DevBuf<int> gpair;
+  DevBuf<int4> citems;  // class-grouped (rotation M2L) items restricted to the shard
+  DevBuf<int> cpair;
+  int n_citems = 0;
   DevBuf<int> gather_cells;
   int n_gather_cells = 0;
   std::vector<int> l2l_off;

@@ -89,6 +89,13 @@ struct Plan {
   std::vector<int4> m2l_gitems;
   DevBuf<int4> d_m2l_gitems;
   DevBuf<int> m2l_gpair;
+  // rotation M2L: pairs grouped by CLASS (same polar-angle table and |D|: the offsets differ
+  // only in the azimuth, applied per vector), items of <= 8 pairs; x = a member offset
+  std::vector<int> h_m2l_off;  // offset id per CSR pair position
+  std::vector<int4> m2l_citems;
+  DevBuf<int4> d_m2l_citems;
+  DevBuf<int> m2l_cpair;
+  std::vector<int> h_m2l_cpair;
   std::vector<int> m2l_tgt_cells;  // target cells with >= 1 M2L source
   DevBuf<int> d_m2l_tgt_cells;
 

@@ -229,6 +229,20 @@ void op_shard_setup(BemOp& op, int rank, int world, const int* tb, const int* sb
   sw.gitems_h = gi;
   sw.gitems.upload(gi.empty() ? std::vector<int4>(1) : gi, s);
   sw.gpair.upload(gp.empty() ? std::vector<int>(1, 0) : gp, s);
+  // the same restriction of the class-grouped items (rotation M2L)
+  {
+    std::vector<int> cp;
+    std::vector<int4> ci;
+    for (const int4& it : pl.m2l_citems) {
+      const int start = (int)cp.size();
+      for (int i = it.y; i < it.z; ++i)
+        if (need[tgt_of[pl.h_m2l_cpair[i]]]) cp.push_back(pl.h_m2l_cpair[i]);
+      if ((int)cp.size() > start) ci.push_back(make_int4(pl.h_m2l_off[cp[start]], start, (int)cp.size(), 0));
+    }
+    sw.n_citems = (int)ci.size();
+    sw.citems.upload(ci.empty() ? std::vector<int4>(1) : ci, s);
+    sw.cpair.upload(cp.empty() ? std::vector<int>(1, 0) : cp, s);
+  }
   // L2L: needed cells whose parent carries a local expansion (plan's pruned lists)
   std::vector<int> l2l_all;
   if (!pl.l2l_level_off.empty() && pl.l2l_level_off.back() > 0) {

@@ -584,23 +584,42 @@ void m2lg_launch(const Plan& plan, const int4* gitems, const int* gpair, int n, 
 // ------------------------------------------------------------------ launchers
 void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
                 cudaStream_t st, const int4* gitems, int n_gitems, const int* cells, int n_cells,
-                const int* gpair) {
-  if (!gpair) gpair = plan.m2l_gpair.get();
+                const int* gpair, const int4* citems, int n_citems, const int* cpair) {
   // part holds one result block per M2L pair (CSR order): n_m2l * C * hcount(p)
+  if (n_cells < 0) n_cells = plan.tgt.n_cells;
+  if (plan.use_rot && p >= M2L_ROT_MIN_P && plan.rot_p >= p) {
+    // class-grouped items (shared polar-angle tables and |D|, per-vector azimuth: ~30 % fewer
+    // warp units) up to p = 10; above, where shared memory limits the resident warps, the
+    // offset-grouped items measured faster (cfg2: p=12 41.7 vs 46.2 us, p=10 32.9 vs 26.7 us)
+    if (p <= 10) {
+      if (!citems) {
+        citems = plan.d_m2l_citems.get();
+        n_citems = (int)plan.m2l_citems.size();
+        cpair = plan.m2l_cpair.get();
+      }
+      launch_m2l_rot(plan, citems, cpair, n_citems, p, C, M, part, st, true);
+    } else {
+      if (!gpair) gpair = plan.m2l_gpair.get();
+      if (!gitems) {
+        gitems = plan.d_m2l_gitems.get();
+        n_gitems = (int)plan.m2l_gitems.size();
+      }
+      launch_m2l_rot(plan, gitems, gpair, n_gitems, p, C, M, part, st, false);
+    }
+  } else {
+  if (!gpair) gpair = plan.m2l_gpair.get();
   if (!gitems) {
     gitems = plan.d_m2l_gitems.get();
     n_gitems = (int)plan.m2l_gitems.size();
   }
-  if (n_cells < 0) n_cells = plan.tgt.n_cells;
-  if (plan.use_rot && p >= M2L_ROT_MIN_P && plan.rot_p >= p) {
-    launch_m2l_rot(plan, gitems, gpair, n_gitems, p, C, M, part, st);
-  } else switch (p) {
+  switch (p) {
 #define G_CASE(PP) case PP: m2lg_launch<PP>(plan, gitems, gpair, n_gitems, C, M, part, st); break;
     G_CASE(0) G_CASE(1) G_CASE(2) G_CASE(3) G_CASE(4) G_CASE(5) G_CASE(6)
     G_CASE(7) G_CASE(8) G_CASE(9) G_CASE(10) G_CASE(11) G_CASE(12) G_CASE(13)
     G_CASE(14) G_CASE(15) G_CASE(16) G_CASE(17) G_CASE(18) G_CASE(19) G_CASE(20)
 #undef G_CASE
     default: throw ArgumentError("M2L: expansion order out of range");
+  }
   }
   if (n_cells > 0) {
     const int CH = C * hcount(p);

@@ -241,6 +241,36 @@ void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
   plan.rot_geo.resize((size_t)std::max(plan.n_offsets, 1) * 3);
   one.resize((size_t)std::max(plan.n_offsets, 1));
   compute_rot_tables(plan.off_d.get(), plan.n_offsets, 0, one.get(), plan.rot_geo.get(), s);
+  if (plan.m2l_citems.empty() && plan.n_m2l > 0) {
+    // classes: (polar-angle table, |D| as the device computed it) -- the members differ only in
+    // the azimuth and share bitwise the same Hankel factors N!/|D|^(N+1)
+    const std::vector<double> geo = plan.rot_geo.download(s);
+    std::map<std::pair<int, double>, int> cls;
+    std::vector<int> cls_of(plan.n_offsets);
+    for (int u = 0; u < plan.n_offsets; ++u)
+      cls_of[u] = cls.emplace(std::make_pair(dir[u], geo[3 * u]), (int)cls.size()).first->second;
+    std::vector<int> gp(plan.n_m2l);
+    for (int k = 0; k < plan.n_m2l; ++k) gp[k] = k;
+    std::stable_sort(gp.begin(), gp.end(), [&](int a, int b) {
+      const int ca = cls_of[plan.h_m2l_off[a]], cb = cls_of[plan.h_m2l_off[b]];
+      return ca != cb ? ca < cb : plan.h_m2l_off[a] < plan.h_m2l_off[b];
+    });
+    for (size_t i = 0; i < gp.size();) {
+      size_t j = i;
+      const int c0 = cls_of[plan.h_m2l_off[gp[i]]];
+      while (j < gp.size() && cls_of[plan.h_m2l_off[gp[j]]] == c0) ++j;
+      const int len = (int)(j - i), nch = (len + 7) / 8;
+      for (int q = 0; q < nch; ++q) {
+        const int lo = (int)i + (int)((int64_t)len * q / nch), hi = (int)i + (int)((int64_t)len * (q + 1) / nch);
+        plan.m2l_citems.push_back(make_int4(plan.h_m2l_off[gp[lo]], lo, hi, 0));
+      }
+      i = j;
+    }
+    plan.h_m2l_cpair = gp;
+    plan.d_m2l_citems.upload(plan.m2l_citems, s);
+    plan.m2l_cpair.upload(gp, s);
+  }
+
   plan.rotf.resize((size_t)nd * rot_frag_size(p));
   build_rot_frag(plan.rot.get(), plan.n_rot_dirs, p, plan.rotf.get(), s);
   plan.rot_aux.resize((size_t)std::max(plan.n_offsets, 1) * rot_aux_size(p));
@@ -305,6 +335,8 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
   plan.m2l_row.upload(plan.h_m2l_row, s);
   plan.m2l_src.upload(plan.h_m2l_src, s);
   plan.m2l_off.upload(offid, s);
+  plan.h_m2l_off = offid;
+  plan.m2l_citems.clear();
   plan.off_d.upload(offd, s);
   plan.h_off = offd;
   plan.m2l_tgt_cells.clear();
