@@ -154,7 +154,7 @@ __device__ __forceinline__ void dmma(double2& d, double a, double b) {
                : "d"(a), "d"(b));
 }
 
-constexpr int ROT_WARPS = 4;
+constexpr int ROT_WARPS = 2;
 constexpr int FRAG_KS_MAX = (P_MAX + 4) / 4;  // k-steps of the largest degree
 static_assert((P_MAX + 8) / 8 <= 3, "row tiles per degree");
 

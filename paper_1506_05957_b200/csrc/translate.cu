@@ -588,24 +588,14 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
   // part holds one result block per M2L pair (CSR order): n_m2l * C * hcount(p)
   if (n_cells < 0) n_cells = plan.tgt.n_cells;
   if (plan.use_rot && p >= M2L_ROT_MIN_P && plan.rot_p >= p) {
-    // class-grouped items (shared polar-angle tables and |D|, per-vector azimuth: ~30 % fewer
-    // warp units) up to p = 10; above, where shared memory limits the resident warps, the
-    // offset-grouped items measured faster (cfg2: p=12 41.7 vs 46.2 us, p=10 32.9 vs 26.7 us)
-    if (p <= 10) {
-      if (!citems) {
-        citems = plan.d_m2l_citems.get();
-        n_citems = (int)plan.m2l_citems.size();
-        cpair = plan.m2l_cpair.get();
-      }
-      launch_m2l_rot(plan, citems, cpair, n_citems, p, C, M, part, st, true);
-    } else {
-      if (!gpair) gpair = plan.m2l_gpair.get();
-      if (!gitems) {
-        gitems = plan.d_m2l_gitems.get();
-        n_gitems = (int)plan.m2l_gitems.size();
-      }
-      launch_m2l_rot(plan, gitems, gpair, n_gitems, p, C, M, part, st, false);
+    // class-grouped items: shared polar-angle tables and |D|, per-vector azimuthal phases;
+    // ~30 % fewer warp units than grouping by offset (cfg2 p=12: 41.4 -> 33.2 us with 2-warp CTAs)
+    if (!citems) {
+      citems = plan.d_m2l_citems.get();
+      n_citems = (int)plan.m2l_citems.size();
+      cpair = plan.m2l_cpair.get();
     }
+    launch_m2l_rot(plan, citems, cpair, n_citems, p, C, M, part, st, true);
   } else {
   if (!gpair) gpair = plan.m2l_gpair.get();
   if (!gitems) {
