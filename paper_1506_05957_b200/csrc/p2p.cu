@@ -548,7 +548,9 @@ void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const dou
   const LapdStage L(max_src, aux.max_leaves, aux.max_tgt);
   static const int nct = std::getenv("FMMBEM_P2P_NCT") ? std::atoi(std::getenv("FMMBEM_P2P_NCT")) : LAPD_CONS;
   const size_t per = L.bytes + (size_t)nct * LAPD_TPT * sizeof(double);
-  static const int want = std::getenv("FMMBEM_P2P_STAGES") ? std::atoi(std::getenv("FMMBEM_P2P_STAGES")) : 3;
+  // 2 stages: measured faster than 3 inside the concurrent step (the far-field kernels share the
+  // SMs' shared memory with this persistent kernel); FMMBEM_P2P_STAGES=3 for a deeper ring
+  static const int want = std::getenv("FMMBEM_P2P_STAGES") ? std::atoi(std::getenv("FMMBEM_P2P_STAGES")) : 2;
   const int nstg = (want >= 3 && 3 * per <= 227 * 1024) ? 3 : 2;
   const size_t smem = nstg * per;
   FMM_REQUIRE(smem <= 227 * 1024, "P2P: source slice too large for shared memory");

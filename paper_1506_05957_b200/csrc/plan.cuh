@@ -7,6 +7,8 @@
 // sets are compared with the reference by content, never by index.
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace fmmbem {
@@ -39,7 +41,13 @@ struct Tree {
   const double* rec = nullptr;  // plan's reciprocal table (common.cuh)
 };
 
-constexpr int P2P_ITEM_SOURCES = 896;   // sources per P2P work item (shared-memory tile)
+constexpr int P2P_ITEM_SOURCES_DEFAULT = 896;  // sources per P2P work item (shared-memory tile)
+// (FMMBEM_P2P_ITEM overrides it, for tuning)
+inline int p2p_item_sources() {
+  static const int v = std::getenv("FMMBEM_P2P_ITEM") ? std::atoi(std::getenv("FMMBEM_P2P_ITEM"))
+                                                      : P2P_ITEM_SOURCES_DEFAULT;
+  return v;
+}
 
 struct P2PItem {
   int tgt_leaf;   // target cell id
