@@ -144,6 +144,9 @@ struct EpiArgs {
   double* y;
   double* ysorted;  // sharded: write (target body - tbody_a) * NC + c instead of y[panel]
   int tbody_a;
+  // one-channel kinds: 0 = whole layer; 1 = near part only (near-field partials + correction,
+  // y = alpha x + beta (near / 4 pi + corr)); 2 = far part only, added: y += beta pot / 4 pi
+  int mode = 0;
 };
 
 // NS threads per target (NS > 1 for the one-channel kinds): slice k takes the
@@ -192,14 +195,15 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
     for (int c = 0; c < NC; ++c) near[c] = 0.0;
     // a leaf's items are consecutive with out_off advancing by nt (plan_make_items)
     const int oo = ib < ie ? a.items[ib].out_off : 0;
-    if (valid)
+    const bool near_part = a.mode != 2;
+    if (valid && near_part)
       for (int it = ib + slice; it < ie; it += NS) {
         const double* pp = a.part + (size_t)(oo + (it - ib) * nt + lt) * NC;
 #pragma unroll
         for (int c = 0; c < NC; ++c) near[c] += pp[c];
       }
     double corr1 = 0.0;
-    if ((KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) && valid) {
+    if ((KIND == K_LAP_SINGLE || KIND == K_LAP_DOUBLE) && valid && near_part) {
       const int2 rr = a.rows[ti];
 #pragma unroll 4
       for (int e = rr.x + slice; e < rr.y; e += NS) corr1 = fma(a.vals[e], a.x[a.cols[e]], corr1);
@@ -233,10 +237,13 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
         __syncthreads();
       }
       if (slice == 0 && valid) {
-        const double layer = far_near / FOUR_PI + corr;
-        const double v = a.alpha * a.x[pn] + a.beta * layer;
-        if (a.ysorted) a.ysorted[ti - a.tbody_a] = v;
-        else a.y[pn] = v;
+        double* yy = a.ysorted ? a.ysorted + (ti - a.tbody_a) : a.y + pn;
+        if (a.mode == 2) {
+          *yy += a.beta * (far_near / FOUR_PI);
+        } else {
+          const double layer = far_near / FOUR_PI + corr;
+          *yy = a.alpha * a.x[pn] + a.beta * layer;
+        }
       }
     } else if (valid) {
       const double xt[3] = {tx, ty, tz};
@@ -462,6 +469,41 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   FMM_CUDA(cudaStreamSynchronize(s));
 }
 
+void launch_layer_epilogue(BemOp& op, const LayerCall& c, bool sharded, cudaStream_t s, int mode) {
+  Plan& pl = op.plan;
+  ShardWork& sw = op.shard;
+  EpiArgs a;
+  a.mode = mode;
+  a.leaves = sharded ? sw.epi_leaves.get() : pl.tgt.leaves.get();
+  a.item_begin = c.dense ? op.dense_item_begin.get() : sharded ? sw.item_begin.get() : pl.tleaf_item_begin.get();
+  a.items = c.dense ? op.dense_items.get() : sharded ? sw.items.get() : pl.d_items.get();
+  a.ysorted = (sharded && !sw.virtual_mode) ? sw.ysend.get() : nullptr;
+  a.tbody_a = sw.tbody_a;
+  const int n_epi = sharded ? sw.n_epi_leaves : pl.tgt.n_leaves;
+  a.part = c.dense ? op.part_dense.get() : op.part.get();
+  a.L = op.L.get();
+  a.path_off = pl.epi_path_off.get();
+  a.path = pl.epi_path.get();
+  a.max_path = pl.max_path;
+  a.p = c.p;
+  a.rowptr = op.near_rowptr.get();
+  a.rows = op.near_rows.get();
+  a.cols = op.near_cols.get();
+  a.vals = c.corr->vals.get();
+  a.x = c.x;
+  a.alpha = c.alpha;
+  a.beta = c.beta;
+  a.y = c.y;
+  if (mode != 1) record(op, ST_EPI, false, s);
+  const bool far = !c.dense && mode != 1;
+  switch (c.kind) {
+    case K_LAP_SINGLE: launch_epilogue<K_LAP_SINGLE>(op, a, far, s, n_epi); break;
+    case K_LAP_DOUBLE: launch_epilogue<K_LAP_DOUBLE>(op, a, far, s, n_epi); break;
+    case K_STOKESLET: launch_epilogue<K_STOKESLET>(op, a, far, s, n_epi); break;
+    default: launch_epilogue<K_STRESSLET>(op, a, far, s, n_epi); break;
+  }
+}
+
 void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   Plan& pl = op.plan;
   ShardWork& sw = op.shard;
@@ -505,7 +547,11 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     launch_p2p((P2PKind)c.kind, S, T, pl.d_items.get(), (int)pl.items.size(), pl.p2p_src.get(),
                op.max_item_sources, w, op.part.get(), sn, pl.p2p_order.get(), &op.p2p_aux,
                op.p2p_sched.get(), op.srec.get(), op.s_panel.get(), c.x);
+  // one-channel kinds: the near part of the epilogue (item partials + correction rows) runs
+  // right behind the near field, concurrently with the far field
   record(op, ST_P2P, true, sn);
+  const bool split_epi = !c.dense && (c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE);
+  if (split_epi) launch_layer_epilogue(op, c, sharded, sn, 1);
   if (!serial) FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
   // far field on the main stream
   if (!c.dense) {
@@ -540,35 +586,9 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     record(op, ST_DOWN, true, s);
   }
   if (!serial) FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
-  EpiArgs a;
-  a.leaves = sharded ? sw.epi_leaves.get() : pl.tgt.leaves.get();
-  a.item_begin = c.dense ? op.dense_item_begin.get() : sharded ? sw.item_begin.get() : pl.tleaf_item_begin.get();
-  a.items = c.dense ? op.dense_items.get() : sharded ? sw.items.get() : pl.d_items.get();
-  a.ysorted = (sharded && !sw.virtual_mode) ? sw.ysend.get() : nullptr;
-  a.tbody_a = sw.tbody_a;
-  const int n_epi = sharded ? sw.n_epi_leaves : pl.tgt.n_leaves;
-  a.part = c.dense ? op.part_dense.get() : op.part.get();
-  a.L = op.L.get();
-  a.path_off = pl.epi_path_off.get();
-  a.path = pl.epi_path.get();
-  a.max_path = pl.max_path;
-  a.p = c.p;
-  a.rowptr = op.near_rowptr.get();
-  a.rows = op.near_rows.get();
-  a.cols = op.near_cols.get();
-  a.vals = c.corr->vals.get();
-  a.x = c.x;
-  a.alpha = c.alpha;
-  a.beta = c.beta;
-  a.y = c.y;
-  record(op, ST_EPI, false, s);
-  switch (c.kind) {
-    case K_LAP_SINGLE: launch_epilogue<K_LAP_SINGLE>(op, a, !c.dense, s, n_epi); break;
-    case K_LAP_DOUBLE: launch_epilogue<K_LAP_DOUBLE>(op, a, !c.dense, s, n_epi); break;
-    case K_STOKESLET: launch_epilogue<K_STOKESLET>(op, a, !c.dense, s, n_epi); break;
-    default: launch_epilogue<K_STRESSLET>(op, a, !c.dense, s, n_epi); break;
-  }
-  if (a.ysorted) shard_exchange_y(op, c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE ? 1 : 3, c.y, s);
+  launch_layer_epilogue(op, c, sharded, s, split_epi ? 2 : 0);
+  const bool ysorted_out = sharded && !sw.virtual_mode;
+  if (ysorted_out) shard_exchange_y(op, c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE ? 1 : 3, c.y, s);
   record(op, ST_EPI, true, s);
   record(op, ST_TOTAL, true, s);
 }
