@@ -186,17 +186,17 @@ def run_reference(args, cfg, mesh, world):
 
 
 # ---------------------------------------------------------------- GPU leg
-M2L_ROT_MIN_P = 6  # csrc/kernels.cuh: rotation-based M2L from this order up
+M2L_ROT_MIN_P = 3  # csrc/kernels.cuh: rotation-based M2L from this order up
 
 
 def m2l_flops(n_pairs, C, p):
     """Algorithmic flops of the M2L formulation the library runs at order p.
 
-    p >= 6, rotation ("point and shoot", m2l_rot.cu): per pair and channel three
+    p >= 3, rotation ("point and shoot", m2l_rot.cu): per pair and channel three
     real products on the real and imaginary parts, stage A and C of order
     (n+1) x (n+1) per degree, stage B (p+1-k) x (p+1-k) per order:
     2 flop x 2 parts x (2 S2 + S2), S2 = sum_{i<=p+1} i^2.
-    p < 6, dense contraction of half-stored outputs with full inputs:
+    p < 3, dense contraction of half-stored outputs with full inputs:
     8 flop per complex MAC x (p+1)(p+2)/2 x (p+1)^2."""
     if p >= M2L_ROT_MIN_P:
         s2 = (p + 1) * (p + 2) * (2 * p + 3) // 6
@@ -352,8 +352,8 @@ def run_ours(args, cfg, mesh, world):
         "peak_source": "live DFMA microkernel on this GPU (MEASURED_PEAKS.json has no fp64 entry)",
         "algorithmic": {
             "p2p": f"{ppf} flop/interaction x {op.plan.p2p_interactions} interactions/apply",
-            "m2l": "rotation M2L (p >= 6): 12 flop x sum_{i<=p+1} i^2 per pair and channel; "
-                   "p < 6: 8 flop/complex MAC x (p+1)(p+2)/2 x (p+1)^2"},
+            "m2l": "rotation M2L (p >= 3): 12 flop x sum_{i<=p+1} i^2 per pair and channel; "
+                   "p < 3: 8 flop/complex MAC x (p+1)(p+2)/2 x (p+1)^2"},
         "stage_ms_per_apply": stages,
         "stage_ms_per_apply_isolated": iso,
         "stage_share_isolated": {k: v / iso["total"] for k, v in iso.items() if k != "total"},
