@@ -381,9 +381,17 @@ int fmmbem_op_gmres(fmmbem_op* h, const double* b, double tol, int p_initial, in
     FMM_CUDA(cudaMemcpyAsync(op.stage_x.get(), b, op.n * sizeof(double), cudaMemcpyHostToDevice, op.s_main));
     gmres_common(h, op.stage_x.get(), tol, p_initial, p_min, relaxed, max_iter, op.stage_y.get(),
                  residuals, orders, n_iter, converged);
-    FMM_CUDA(cudaMemcpyAsync(x, op.stage_y.get(), op.n * sizeof(double), cudaMemcpyDeviceToHost, op.s_main));
+    // x through a pinned staging buffer (a pageable D2H copy is staged by the driver, slower)
+    if (op.xpin_cap < op.n) {
+      if (op.xpin_h) FMM_CUDA(cudaFreeHost(op.xpin_h));
+      FMM_CUDA(cudaHostAlloc(&op.xpin_h, op.n * sizeof(double), cudaHostAllocDefault));
+      op.xpin_cap = op.n;
+    }
+    FMM_CUDA(cudaMemcpyAsync(op.xpin_h, op.stage_y.get(), op.n * sizeof(double), cudaMemcpyDeviceToHost,
+                             op.s_main));
     FMM_CUDA(cudaEventRecord(op.call_ev[1], op.s_main));
     FMM_CUDA(cudaStreamSynchronize(op.s_main));
+    std::memcpy(x, op.xpin_h, op.n * sizeof(double));
     float ms = 0.f;
     FMM_CUDA(cudaEventElapsedTime(&ms, op.call_ev[0], op.call_ev[1]));
     op.last_call_ms = ms;

@@ -367,6 +367,7 @@ void record(BemOp& op, int stage, bool end, cudaStream_t s) {
 BemOp::~BemOp() {
   for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
   if (mbox_h) cudaFreeHost(mbox_h);
+  if (xpin_h) cudaFreeHost(xpin_h);
   if (mflag_h) cudaFreeHost(mflag_h);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);

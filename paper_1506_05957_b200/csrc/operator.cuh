@@ -134,6 +134,8 @@ struct BemOp {
   // sequence number straight into pinned host memory; the host spins on it
   // instead of a copy + stream synchronisation per iteration
   double* mbox_h = nullptr;                 // [mbox_cap] values
+  double* xpin_h = nullptr;                 // pinned staging of the host solution (n)
+  int64_t xpin_cap = 0;
   double* mbox_d = nullptr;
   unsigned long long* mflag_h = nullptr;    // sequence flag
   unsigned long long* mflag_d = nullptr;
