@@ -309,30 +309,39 @@ __global__ void __launch_bounds__(ACT) k_arnoldi_cluster(int n, int k, const dou
 // ||b|| on one cluster (n <= ACL * ACT * AE): written to the device scalar and posted to the
 // host mailbox slot, read by the host together with the first Arnoldi column
 __global__ void __launch_bounds__(ACT) k_norm_cluster(int n, const double* __restrict__ b, double* out,
-                                                      double* mbox) {
+                                                      double* mbox, double* v, double* v2) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ double sh[ACT / 32];
   __shared__ double part[ACL];
   const int rank = (int)cluster.block_rank();
   const int t = rank * ACT + threadIdx.x;
+  double br[AE];
   double acc = 0.0;
 #pragma unroll
   for (int e = 0; e < AE; ++e) {
     const int i = t + e * ACL * ACT;
-    if (i < n) acc = fma(b[i], b[i], acc);
+    br[e] = i < n ? b[i] : 0.0;
+    acc = fma(br[e], br[e], acc);
   }
   const double bs = block_sum(acc, sh);
   if (threadIdx.x == 0)
 #pragma unroll
     for (int r = 0; r < ACL; ++r) *cluster.map_shared_rank(part + rank, r) = bs;
   cluster.sync();
-  if (t == 0) {
-    double tot = 0.0;
+  double tot = 0.0;
 #pragma unroll
-    for (int r = 0; r < ACL; ++r) tot += part[r];
-    *out = mbox[0] = sqrt(tot);
+  for (int r = 0; r < ACL; ++r) tot += part[r];
+  const double nb = sqrt(tot);
+  if (t == 0) {
+    *out = mbox[0] = nb;
     __threadfence_system();
+  }
+  // v_0 = b / ||b|| (and the first mat-vec's input), as k_scale (b = 0: zeros)
+#pragma unroll
+  for (int e = 0; e < AE; ++e) {
+    const int i = t + e * ACL * ACT;
+    if (i < n) v[i] = v2[i] = nb > 0.0 ? br[e] / nb : 0.0;
   }
 }
 
@@ -406,10 +415,14 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     cfg.numAttrs = 1;
     return cfg;
   };
+  DevBuf<double>& V = op.g_basis;
+  V.ensure((size_t)(max_iter + 1) * n);
+  bool fused_scale = false;  // the cluster norm also writes v_0 (k_scale otherwise)
   if (n <= (int64_t)ACL * ACT * AE) {
     cudaLaunchAttribute at[1];
     cudaLaunchConfig_t cfg = cluster_cfg(at);
-    FMM_CUDA(cudaLaunchKernelEx(&cfg, k_norm_cluster, (int)n, b, nb, nb_box));
+    FMM_CUDA(cudaLaunchKernelEx(&cfg, k_norm_cluster, (int)n, b, nb, nb_box, V.get(), op.x_in.get()));
+    fused_scale = true;
   } else {
     k_norm<<<RB, RT, 0, s>>>(n, const_cast<double*>(b), nullptr, nullptr, partials.get(), counter.get(), nb,
                              nb_box, nullptr, 0);
@@ -431,10 +444,10 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     FMM_CUDA(cudaStreamSynchronize(s));
     if (read_norm_b()) return res;
   }
-  DevBuf<double>& V = op.g_basis;
-  V.ensure((size_t)(max_iter + 1) * n);
-  k_scale<<<RB, RT, 0, s>>>(n, b, nb, V.get(), op.x_in.get());
-  op.kernel_launches += 1;
+  if (!fused_scale) {
+    k_scale<<<RB, RT, 0, s>>>(n, b, nb, V.get(), op.x_in.get());
+    op.kernel_launches += 1;
+  }
   std::vector<double> H((size_t)(max_iter + 1) * std::max(max_iter, 1), 0.0);
   auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * max_iter + j]; };
   std::vector<double> cs(max_iter), sn(max_iter), g(max_iter + 1, 0.0), hcol(max_iter + 2);
