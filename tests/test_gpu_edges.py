@@ -90,3 +90,26 @@ def test_small_relaxed_solves_match_the_oracle(formulation):
     rr = O.gmres(ref.apply, b, O.RelaxationSchedule(p0, pmin, 1e-6, True), 1e-6, 100)
     assert abs(res.n_iterations - rr.n_iterations) <= 1
     assert rel_l2(res.x, rr.x) <= 1e-6
+
+
+@pytest.mark.parametrize("theta", [0.3, 0.7])
+def test_other_opening_angles(theta):
+    from paper_1506_05957_b200 import make_icosphere
+
+    op, ref = _pair(make_icosphere(2), "laplace_second", n_crit=16, theta=theta)
+    x = np.random.default_rng(8).uniform(-1.0, 1.0, op.shape[0])
+    for p in (4, 9):
+        y, yr = op.apply(x, p), ref.apply(x, p)
+        assert rel_l2(y, yr) <= MATVEC_TOL, (theta, p, rel_l2(y, yr))
+
+
+@pytest.mark.parametrize("formulation", ["laplace_second", "stokes"])
+def test_deep_tree_n_crit_1(formulation):
+    # one point per leaf where possible: deep trees, long root paths, many tiny P2P items
+    from paper_1506_05957_b200 import make_icosphere
+
+    op, ref = _pair(make_icosphere(1), formulation, n_crit=1)
+    x = np.random.default_rng(9).uniform(-1.0, 1.0, op.shape[0])
+    for p in (3, 10):
+        y, yr = op.apply(x, p), ref.apply(x, p)
+        assert rel_l2(y, yr) <= MATVEC_TOL, (formulation, p, rel_l2(y, yr))
