@@ -113,3 +113,16 @@ def test_deep_tree_n_crit_1(formulation):
     for p in (3, 10):
         y, yr = op.apply(x, p), ref.apply(x, p)
         assert rel_l2(y, yr) <= MATVEC_TOL, (formulation, p, rel_l2(y, yr))
+
+
+def test_double_layer_far_from_the_origin():
+    # 8 rotated red-blood-cell surfaces on a 2x2x2 lattice (|x| up to ~13 um, level-3 cells):
+    # the expanded-form near field centres on the target leaf, so its cancellation does not
+    # grow with the distance to the origin
+    from paper_1506_05957_b200 import make_rbc_lattice
+
+    op, ref = _pair(make_rbc_lattice(2, level=3), "laplace_second", n_crit=64)
+    x = np.random.default_rng(10).uniform(-1.0, 1.0, op.shape[0])
+    for p in (5, 12):
+        y, yr = op.apply(x, p), ref.apply(x, p)
+        assert rel_l2(y, yr) <= MATVEC_TOL, (p, rel_l2(y, yr))
