@@ -199,7 +199,10 @@ k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __rest
 // largest-first order from a global counter and stage item k+1 (leaf table, transformed
 // sources, every target's own-source slot) into one of two shared-memory stages while the
 // LAPD_CONS consumer threads run the interaction loop on item k.  Stages are handed over
-// with named barriers (FULL: producers arrive, consumers wait; EMPTY: the reverse).
+// through barriers: FULL is a shared-memory mbarrier per stage (every producer thread arrives,
+// consumer warps only wait on its phase, so no consumer warp waits for another — the last
+// warp's reduction of item k overlaps the other warps' item k + 1); EMPTY is a named barrier
+// (consumers arrive, producers sync).
 constexpr int LAPD_TPT = 4;
 constexpr int LAPD_CONS = 256;
 constexpr int LAPD_PROD = 128;
@@ -210,6 +213,27 @@ __device__ __forceinline__ void bar_sync(int id, int n) {
 }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "MBW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MBW_%=;\n"
+      "}\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -273,7 +297,11 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
   double* red = reinterpret_cast<double*>(smem + NSTG * L.bytes);  // [NSTG][NCT * TPT] group partials
   __shared__ int s_idx;
   __shared__ unsigned s_done[NSTG];  // consumer warps done with the stage's item
-  if (threadIdx.x < NSTG) s_done[threadIdx.x] = 0u;
+  __shared__ unsigned long long s_full[NSTG];  // FULL mbarriers (NPT arrivals per phase)
+  if (threadIdx.x < NSTG) {
+    s_done[threadIdx.x] = 0u;
+    mbar_init(&s_full[threadIdx.x], NPT);
+  }
   __syncthreads();
   if (threadIdx.x >= NCT) {
     // ------------------------------------------------------------------ producers
@@ -302,7 +330,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
       if (pt == 0) nxt = atomicAdd(sched, 1u);
       if (cur >= n_items) {
         if (pt == 0) hdr[0] = 0;
-        bar_arrive(BAR_FULL0 + st, ALL);
+        mbar_arrive(&s_full[st]);
         break;
       }
       const LapdHdr H = hdrs[cur];
@@ -370,7 +398,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
         }
       }
       if (pt == 0) TR(k, 2);
-      bar_arrive(BAR_FULL0 + st, ALL);
+      mbar_arrive(&s_full[st]);
     }
     // match the consumers' EMPTY arrivals of the last NSTG - 1 items
     for (int j = max(0, k - NSTG + 1); j < k; ++j) bar_sync(BAR_EMPTY0 + j % NSTG, ALL);
@@ -395,7 +423,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
     const double2* tg = reinterpret_cast<const double2*>(base + L.tgt);
     const int* hdr = slot + 2 * max_tgt;
     if (threadIdx.x == 0) TR(k, 3);
-    bar_sync(BAR_FULL0 + st, ALL);
+    mbar_wait(&s_full[st], (unsigned)(k / NSTG) & 1u);
     if (threadIdx.x == 0) TR(k, 4);
     if (hdr[0] == 0) break;
     const int ns = hdr[1], nt = hdr[2], out_off = hdr[3], nspec = hdr[4];
