@@ -303,102 +303,123 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
     mbar_init(&s_full[threadIdx.x], NPT);
   }
   __syncthreads();
+  // stage item `cur` into stage st with threads tid < nthr (false: the schedule is exhausted)
+  auto stage = [&](int cur, int st, int tid, int nthr, bool all) -> bool {
+    unsigned char* base = smem + st * L.bytes;
+    double2* sh2 = reinterpret_cast<double2*>(base);
+    int4* ltab = reinterpret_cast<int4*>(base + L.ltab);
+    int* slot = reinterpret_cast<int*>(base + L.slot);
+    double2* tg = reinterpret_cast<double2*>(base + L.tgt);
+    int* spec = slot + max_tgt;  // tile positions (item order) of the targets' own sources
+    int* hdr = spec + max_tgt;   // live (0: done), ns, nt, out_off, nspec
+    if (cur >= n_items) {
+      if (tid == 0) hdr[0] = 0;
+      return false;
+    }
+    const LapdHdr H = hdrs[cur];
+    for (int q = tid; q < H.nl; q += nthr) ltab[q] = gl_ltab[H.pair_begin + q];
+    for (int lt = tid; lt < H.nt; lt += nthr) {
+      slot[lt] = gl_slot[H.out_off + lt];
+      if (lt < H.nspec) spec[lt] = gl_spec[H.out_off + lt];
+      const double x = T.px[H.t0 + lt] - H.cx, y = T.py[H.t0 + lt] - H.cy, z = T.pz[H.t0 + lt] - H.cz;
+      tg[lt] = make_double2(x, y);
+      tg[max_tgt + lt] = make_double2(z, fma(x, x, fma(y, y, z * z)));
+    }
+    if (tid == 0) {
+      hdr[0] = 1;
+      hdr[1] = H.ns;
+      hdr[2] = H.nt;
+      hdr[3] = H.out_off;
+      hdr[4] = H.nspec;
+    }
+    if (all) __syncthreads();
+    else bar_sync(BAR_PROD, NPT);
+    // flattened over the tile: 4 sources per thread per round, loads issued before use
+    for (int i0 = tid; i0 < H.ns; i0 += 4 * nthr) {
+      double2 v[4][3];
+      int pn[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = min(i0 + u * nthr, H.ns - 1);
+        int lo = 0, hi = H.nl - 1;  // last leaf with offset <= i
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ltab[mid].z <= i) lo = mid;
+          else hi = mid - 1;
+        }
+        const int4 e = ltab[lo];
+        const int gi = e.x + i - e.z;
+        const size_t g = (size_t)gi * 3;
+        v[u][0] = srec[g];
+        v[u][1] = srec[g + 1];
+        v[u][2] = srec[g + 2];
+        pn[u] = s_panel[gi];
+      }
+      double xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = xd[pn[u]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nthr;
+        if (i >= H.ns) break;
+        // destination: own sources first (rank among them), the rest compacted after
+        int r = 0, hi = H.nspec;  // r = number of own sources at tile positions < i
+        while (r < hi) {
+          const int mid = (r + hi) >> 1;
+          if (spec[mid] < i) r = mid + 1;
+          else hi = mid;
+        }
+        const int dst = (r < H.nspec && spec[r] == i) ? r : H.nspec + i - r;
+        const double sx = v[u][0].x - H.cx, sy = v[u][0].y - H.cy, sz = v[u][1].x - H.cz;
+        // dipole d = (w n) x[panel] (bemop.py:188-203, 213-216)
+        const double dx = v[u][1].y * xv[u], dy = v[u][2].x * xv[u], dz = v[u][2].y * xv[u];
+        const double ss = fma(sx, sx, fma(sy, sy, sz * sz));
+        const double ds = fma(dx, sx, fma(dy, sy, dz * sz));
+        sh2[dst] = make_double2(-2.0 * sx, -2.0 * sy);
+        sh2[max_src + dst] = make_double2(-2.0 * sz, ss);
+        sh2[2 * max_src + dst] = make_double2(dx, dy);
+        sh2[3 * max_src + dst] = make_double2(dz, -ds);
+      }
+    }
+    return true;
+  };
+  // prologue: the whole CTA stages its first item (nothing to overlap it with yet); the
+  // producers then hand it over through FULL like every later item
+  unsigned nxt = 0;
+  if (threadIdx.x == NCT) {
+    TR(0, 0);
+    nxt = atomicAdd(sched, 1u);
+  }
+  const bool live0 = stage(blockIdx.x, 0, threadIdx.x, ALL, true);
+  __syncthreads();
   if (threadIdx.x >= NCT) {
     // ------------------------------------------------------------------ producers
     // schedule position blockIdx.x first, then positions gridDim.x + atomicAdd(sched) (the next
     // one requested while the current item is staged)
     const int pt = threadIdx.x - NCT;
-    int k = 0, cur = blockIdx.x;
-    unsigned nxt = 0;
-    for (;; ++k) {
-      const int st = k % NSTG;
-      unsigned char* base = smem + st * L.bytes;
-      double2* sh2 = reinterpret_cast<double2*>(base);
-      int4* ltab = reinterpret_cast<int4*>(base + L.ltab);
-      int* slot = reinterpret_cast<int*>(base + L.slot);
-      double2* tg = reinterpret_cast<double2*>(base + L.tgt);
-      int* spec = slot + max_tgt;  // tile positions (item order) of the targets' own sources
-      int* hdr = spec + max_tgt;   // live (0: done), ns, nt, out_off, nspec
-      if (pt == 0) TR(k, 0);
-      if (k >= NSTG) bar_sync(BAR_EMPTY0 + st, ALL);
-      if (pt == 0) TR(k, 1);
-      if (k > 0) {
+    if (pt == 0) {
+      TR(0, 1);
+      TR(0, 2);
+    }
+    mbar_arrive(&s_full[0]);
+    int k = 1;
+    if (live0) {
+      for (;; ++k) {
+        const int st = k % NSTG;
+        if (pt == 0) TR(k, 0);
+        if (k >= NSTG) bar_sync(BAR_EMPTY0 + st, ALL);
+        if (pt == 0) TR(k, 1);
         if (pt == 0) s_idx = (int)(gridDim.x + nxt);
         bar_sync(BAR_PROD, NPT);
-        cur = s_idx;
-      }
-      if (pt == 0) nxt = atomicAdd(sched, 1u);
-      if (cur >= n_items) {
-        if (pt == 0) hdr[0] = 0;
+        const int cur = s_idx;
+        if (pt == 0) nxt = atomicAdd(sched, 1u);
+        const bool live = stage(cur, st, pt, NPT, false);
+        if (live && pt == 0) TR(k, 2);
         mbar_arrive(&s_full[st]);
-        break;
+        if (!live) break;
       }
-      const LapdHdr H = hdrs[cur];
-      for (int q = pt; q < H.nl; q += NPT) ltab[q] = gl_ltab[H.pair_begin + q];
-      for (int lt = pt; lt < H.nt; lt += NPT) {
-        slot[lt] = gl_slot[H.out_off + lt];
-        if (lt < H.nspec) spec[lt] = gl_spec[H.out_off + lt];
-        const double x = T.px[H.t0 + lt] - H.cx, y = T.py[H.t0 + lt] - H.cy, z = T.pz[H.t0 + lt] - H.cz;
-        tg[lt] = make_double2(x, y);
-        tg[max_tgt + lt] = make_double2(z, fma(x, x, fma(y, y, z * z)));
-      }
-      if (pt == 0) {
-        hdr[0] = 1;
-        hdr[1] = H.ns;
-        hdr[2] = H.nt;
-        hdr[3] = H.out_off;
-        hdr[4] = H.nspec;
-      }
-      bar_sync(BAR_PROD, NPT);
-      // flattened over the tile: 4 sources per thread per round, loads issued before use
-      for (int i0 = pt; i0 < H.ns; i0 += 4 * NPT) {
-        double2 v[4][3];
-        int pn[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = min(i0 + u * NPT, H.ns - 1);
-          int lo = 0, hi = H.nl - 1;  // last leaf with offset <= i
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (ltab[mid].z <= i) lo = mid;
-            else hi = mid - 1;
-          }
-          const int4 e = ltab[lo];
-          const int gi = e.x + i - e.z;
-          const size_t g = (size_t)gi * 3;
-          v[u][0] = srec[g];
-          v[u][1] = srec[g + 1];
-          v[u][2] = srec[g + 2];
-          pn[u] = s_panel[gi];
-        }
-        double xv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) xv[u] = xd[pn[u]];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + u * NPT;
-          if (i >= H.ns) break;
-          // destination: own sources first (rank among them), the rest compacted after
-          int r = 0, hi = H.nspec;  // r = number of own sources at tile positions < i
-          while (r < hi) {
-            const int mid = (r + hi) >> 1;
-            if (spec[mid] < i) r = mid + 1;
-            else hi = mid;
-          }
-          const int dst = (r < H.nspec && spec[r] == i) ? r : H.nspec + i - r;
-          const double sx = v[u][0].x - H.cx, sy = v[u][0].y - H.cy, sz = v[u][1].x - H.cz;
-          // dipole d = (w n) x[panel] (bemop.py:188-203, 213-216)
-          const double dx = v[u][1].y * xv[u], dy = v[u][2].x * xv[u], dz = v[u][2].y * xv[u];
-          const double ss = fma(sx, sx, fma(sy, sy, sz * sz));
-          const double ds = fma(dx, sx, fma(dy, sy, dz * sz));
-          sh2[dst] = make_double2(-2.0 * sx, -2.0 * sy);
-          sh2[max_src + dst] = make_double2(-2.0 * sz, ss);
-          sh2[2 * max_src + dst] = make_double2(dx, dy);
-          sh2[3 * max_src + dst] = make_double2(dz, -ds);
-        }
-      }
-      if (pt == 0) TR(k, 2);
-      mbar_arrive(&s_full[st]);
+    } else {
+      k = 0;
     }
     // match the consumers' EMPTY arrivals of the last NSTG - 1 items
     for (int j = max(0, k - NSTG + 1); j < k; ++j) bar_sync(BAR_EMPTY0 + j % NSTG, ALL);
