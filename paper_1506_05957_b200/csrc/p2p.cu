@@ -206,6 +206,10 @@ k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __rest
 constexpr int LAPD_TPT = 4;
 constexpr int LAPD_CONS = 256;
 constexpr int LAPD_PROD = 128;
+#ifndef LAPD_SPR
+#define LAPD_SPR 4
+#endif
+constexpr int SPR = LAPD_SPR;  // sources per staging thread per round (loads in flight)
 enum : int { BAR_FULL0 = 1, BAR_EMPTY0 = 5, BAR_PROD = 9 };  // up to 4 stages
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
@@ -334,12 +338,12 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
     }
     if (all) __syncthreads();
     else bar_sync(BAR_PROD, NPT);
-    // flattened over the tile: 4 sources per thread per round, loads issued before use
-    for (int i0 = tid; i0 < H.ns; i0 += 4 * nthr) {
-      double2 v[4][3];
-      int pn[4];
+    // flattened over the tile: SPR sources per thread per round, loads issued before use
+    for (int i0 = tid; i0 < H.ns; i0 += SPR * nthr) {
+      double2 v[SPR][3];
+      int pn[SPR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < SPR; ++u) {
         const int i = min(i0 + u * nthr, H.ns - 1);
         int lo = 0, hi = H.nl - 1;  // last leaf with offset <= i
         while (lo < hi) {
@@ -355,11 +359,11 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
         v[u][2] = srec[g + 2];
         pn[u] = s_panel[gi];
       }
-      double xv[4];
+      double xv[SPR];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xv[u] = xd[pn[u]];
+      for (int u = 0; u < SPR; ++u) xv[u] = xd[pn[u]];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < SPR; ++u) {
         const int i = i0 + u * nthr;
         if (i >= H.ns) break;
         // destination: own sources first (rank among them), the rest compacted after
