@@ -530,11 +530,18 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   }
   DevBuf<double>& yd = op.g_y;
   yd.ensure(y.size());
-  FMM_CUDA(cudaMemcpyAsync(yd.get(), y.data(), y.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (op.ypin_cap < (int)y.size()) {  // pinned: the copy is truly asynchronous
+    if (op.ypin_h) FMM_CUDA(cudaFreeHost(op.ypin_h));
+    op.ypin_cap = std::max((int)y.size(), max_iter);
+    FMM_CUDA(cudaHostAlloc(&op.ypin_h, op.ypin_cap * sizeof(double), cudaHostAllocDefault));
+  }
+  std::copy(y.begin(), y.end(), op.ypin_h);
+  FMM_CUDA(cudaMemcpyAsync(yd.get(), op.ypin_h, y.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   k_combine<<<RB, RT, 0, s>>>(n, m, V.get(), yd.get(), x);
   FMM_LAUNCH_CHECK();
   op.kernel_launches += 1;
-  FMM_CUDA(cudaStreamSynchronize(s));
+  // x is complete in stream order on op.s_main; the callers (capi.cu) record their end event,
+  // queue the D2H copy if any and synchronise once
   return res;
 }
 

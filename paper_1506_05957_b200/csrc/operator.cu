@@ -368,6 +368,7 @@ BemOp::~BemOp() {
   for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
   if (mbox_h) cudaFreeHost(mbox_h);
   if (xpin_h) cudaFreeHost(xpin_h);
+  if (ypin_h) cudaFreeHost(ypin_h);
   if (mflag_h) cudaFreeHost(mflag_h);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);

@@ -135,6 +135,8 @@ struct BemOp {
   // instead of a copy + stream synchronisation per iteration
   double* mbox_h = nullptr;                 // [mbox_cap] values
   double* xpin_h = nullptr;                 // pinned staging of the host solution (n)
+  double* ypin_h = nullptr;                 // pinned staging of the least-squares solution y
+  int ypin_cap = 0;
   int64_t xpin_cap = 0;
   double* mbox_d = nullptr;
   unsigned long long* mflag_h = nullptr;    // sequence flag
