@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -38,6 +40,34 @@ struct ArgumentError : std::invalid_argument {
   } while (0)
 
 #define FMM_LAUNCH_CHECK() FMM_CUDA(cudaGetLastError())
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may start while the
+// previous kernel on its stream drains; it must call pdl_wait() before reading that
+// kernel's output (a no-op when launched normally).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FMMBEM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  FMM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 #define FMM_REQUIRE(cond, msg)                  \
   do {                                          \

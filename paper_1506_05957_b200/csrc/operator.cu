@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
   // every path cell's local expansion (the leaf, then its ancestors with M2L terms) and its
   // centre, staged once (the L2P loop below then touches no global memory)
   __shared__ double s_cc[3 * 24];
+  pdl_wait();  // L (the M2L gather) and the partials are complete past this point
   for (int i = threadIdx.x; i < np * C * H; i += blockDim.x) {
     const int k = i / (C * H), r = i - k * (C * H);
     sL[i] = a.L[(size_t)a.path[pb + k] * C * H + r];
@@ -300,7 +301,7 @@ void launch_epilogue(BemOp& op, const EpiArgs& a, bool far, cudaStream_t s, int 
     FMM_REQUIRE(smem <= 227 * 1024, "epilogue: root paths too long for shared memory");
     FMM_CUDA(cudaFuncSetAttribute(k_epilogue<KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)std::min<size_t>(most, 227 * 1024)));
-    k_epilogue<KIND, true><<<dim3(nl, tiles), EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
+    launch_pdl(k_epilogue<KIND, true>, dim3(nl, tiles), dim3(EPI_TGT * NS), smem, s, tree_dev(op.plan.tgt), a);
   } else {
     k_epilogue<KIND, false><<<dim3(nl, tiles), EPI_TGT * NS, smem, s>>>(tree_dev(op.plan.tgt), a);
   }

@@ -519,6 +519,7 @@ k_m2l_gather(const int* __restrict__ cells, const int* __restrict__ row, int CH,
   const int t = blockIdx.y * 64 + (threadIdx.x & 63), q = threadIdx.x >> 6;
   const int i0 = row[cell], i1 = row[cell + 1];
   double2 s = make_double2(0.0, 0.0);
+  pdl_wait();  // the M2L results are complete past this point
   if (t < CH)
     for (int i = i0 + q; i < i1; i += 4) s = cadd(s, pout[(size_t)i * CH + t]);
   red[q][threadIdx.x & 63] = s;
@@ -614,7 +615,7 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
   if (n_cells > 0) {
     const int CH = C * hcount(p);
     dim3 grid(n_cells, (CH + 63) / 64);
-    k_m2l_gather<<<grid, 256, 0, st>>>(cells, plan.m2l_row.get(), CH, part, L);
+    launch_pdl(k_m2l_gather, grid, dim3(256), 0, st, cells, plan.m2l_row.get(), CH, (const double2*)part, L);
   }
   FMM_LAUNCH_CHECK();
 }
