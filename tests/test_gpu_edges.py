@@ -126,3 +126,16 @@ def test_double_layer_far_from_the_origin():
     for p in (5, 12):
         y, yr = op.apply(x, p), ref.apply(x, p)
         assert rel_l2(y, yr) <= MATVEC_TOL, (p, rel_l2(y, yr))
+
+
+@pytest.mark.parametrize("n_crit", [300, 700])
+def test_fewer_near_field_items_than_ctas(n_crit):
+    # a handful of large leaves: the persistent near field has fewer work items than CTAs
+    # (idle CTAs take the empty-schedule path of the stage hand-off), items near the source cap
+    from paper_1506_05957_b200 import make_icosphere
+
+    op, ref = _pair(make_icosphere(3), "laplace_second", n_crit=n_crit)
+    x = np.random.default_rng(11).uniform(-1.0, 1.0, op.shape[0])
+    for p in (3, 9):
+        y, yr = op.apply(x, p), ref.apply(x, p)
+        assert rel_l2(y, yr) <= MATVEC_TOL, (n_crit, p, rel_l2(y, yr))
