@@ -71,7 +71,9 @@ __device__ __forceinline__ void interact(double rx, double ry, double rz, const 
     return;
   }
   const double d2 = fma(rx, rx, fma(ry, ry, rz * rz));
-  const double inv = d2 > 0.0 ? rsqrt_nr(d2) : 0.0;
+  // d2 >= +0 always: the coincident-pair mask (fmm.py:403) as an integer compare of the bit
+  // pattern (integer pipe) instead of a DSETP on the FP64 pipe
+  const double inv = __double_as_longlong(d2) > 0 ? rsqrt_nr(d2) : 0.0;
   if (K == P2PKind::LAP_Q) {
     acc[0] = fma(wv[0], inv, acc[0]);
   } else if (K == P2PKind::LAP_D) {
@@ -79,11 +81,12 @@ __device__ __forceinline__ void interact(double rx, double ry, double rz, const 
     const double inv3 = inv * inv * inv;
     acc[0] = fma(rn, inv3, acc[0]);
   } else if (K == P2PKind::STOKESLET) {
+    // f / r + r (r.f) / r^3 = (f + r (r.f) / r^2) / r: 8 DP instructions after inv
     const double rf = fma(rx, wv[0], fma(ry, wv[1], rz * wv[2]));
-    const double s = rf * (inv * inv * inv);
-    acc[0] = fma(wv[0], inv, fma(rx, s, acc[0]));
-    acc[1] = fma(wv[1], inv, fma(ry, s, acc[1]));
-    acc[2] = fma(wv[2], inv, fma(rz, s, acc[2]));
+    const double t = rf * (inv * inv);
+    acc[0] = fma(fma(rx, t, wv[0]), inv, acc[0]);
+    acc[1] = fma(fma(ry, t, wv[1]), inv, acc[1]);
+    acc[2] = fma(fma(rz, t, wv[2]), inv, acc[2]);
   } else {
     // stresslet contracted with the source normal: 6 r (r.f)(r.n) / r^5 (kernels.py:51-58)
     const double rf = fma(rx, wv[0], fma(ry, wv[1], rz * wv[2]));
