@@ -144,7 +144,7 @@ struct EpiArgs {
   double* y;
   double* ysorted;  // sharded: write (target body - tbody_a) * NC + c instead of y[panel]
   int tbody_a;
-  // one-channel kinds: 0 = whole layer; 1 = near part only (near-field partials + correction,
+  // 0 = whole layer; 1 = near part only (near-field partials + correction,
   // y = alpha x + beta (near / 4 pi + corr)); 2 = far part only, added: y += beta pot / 4 pi
   int mode = 0;
 };
@@ -263,6 +263,13 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
         }
         u[i] += near[i];
       }
+      if (a.mode == 2) {  // far part only: the near part (k_block_near) already wrote y
+        for (int r = 0; r < 3; ++r) {
+          double* yy = a.ysorted ? a.ysorted + 3 * (ti - a.tbody_a) + r : a.y + 3 * pn + r;
+          *yy += a.beta * u[r];
+        }
+        return;
+      }
       double corr[3] = {0.0, 0.0, 0.0};
       for (int e = a.rowptr[pn]; e < a.rowptr[pn + 1]; ++e) {
         const double* blk = a.vals + (size_t)e * 9;
@@ -276,6 +283,47 @@ __global__ void __launch_bounds__(EPI_TGT * epi_slices<KIND>()) k_epilogue(TreeD
         else a.y[3 * pn + r] = v;
       }
     }
+  }
+}
+
+// Near part of the 3-component (Stokes) layers, y = alpha x + beta (near + C x): one warp per
+// target, its lanes over the near-field item partials and the 3x3 correction blocks of its
+// row (a streaming block-CSR row product instead of one thread walking the whole row), the
+// lanes' sums combined by a fixed xor-shuffle tree (bitwise reproducible).  Runs on the near
+// stream beside the far field; the far epilogue (mode 2) then adds beta * u_far.
+constexpr int BN_WARPS = 8;
+__global__ void __launch_bounds__(BN_WARPS * 32) k_block_near(TreeDev T, EpiArgs a) {
+  const int li = blockIdx.x, leaf = a.leaves[li];
+  const int t0 = T.body_start[leaf], nt = T.body_count[leaf];
+  const int lt = blockIdx.y * BN_WARPS + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (lt >= nt) return;  // warp-uniform
+  const int ti = t0 + lt;
+  const int ib = a.item_begin[li], ie = a.item_begin[li + 1];
+  const int oo = ib < ie ? a.items[ib].out_off : 0;
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int it = ib + lane; it < ie; it += 32) {
+    const double* pp = a.part + (size_t)(oo + (it - ib) * nt + lt) * 3;
+    v[0] += pp[0];
+    v[1] += pp[1];
+    v[2] += pp[2];
+  }
+  const int2 rr = a.rows[ti];
+  for (int e = rr.x + lane; e < rr.y; e += 32) {
+    const double* blk = a.vals + (size_t)e * 9;
+    const double* xs = a.x + 3 * (size_t)a.cols[e];
+    const double x0 = xs[0], x1 = xs[1], x2 = xs[2];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) v[r] = fma(blk[3 * r], x0, fma(blk[3 * r + 1], x1, fma(blk[3 * r + 2], x2, v[r])));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
+  if (lane < 3) {
+    const int pn = T.perm[ti];
+    const double val = a.alpha * a.x[3 * pn + lane] + a.beta * (lane == 0 ? v[0] : lane == 1 ? v[1] : v[2]);
+    if (a.ysorted) a.ysorted[3 * (ti - a.tbody_a) + lane] = val;
+    else a.y[3 * pn + lane] = val;
   }
 }
 
@@ -499,6 +547,12 @@ void launch_layer_epilogue(BemOp& op, const LayerCall& c, bool sharded, cudaStre
   a.y = c.y;
   if (mode != 1) record(op, ST_EPI, false, s);
   const bool far = !c.dense && mode != 1;
+  if (mode == 1 && c.kind == K_STOKESLET) {
+    const int tiles = (std::max(op.plan.tgt.max_leaf_count, 1) + BN_WARPS - 1) / BN_WARPS;
+    if (n_epi > 0) k_block_near<<<dim3(n_epi, tiles), BN_WARPS * 32, 0, s>>>(tree_dev(op.plan.tgt), a);
+    FMM_LAUNCH_CHECK();
+    return;
+  }
   switch (c.kind) {
     case K_LAP_SINGLE: launch_epilogue<K_LAP_SINGLE>(op, a, far, s, n_epi); break;
     case K_LAP_DOUBLE: launch_epilogue<K_LAP_DOUBLE>(op, a, far, s, n_epi); break;
@@ -553,7 +607,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   // one-channel kinds: the near part of the epilogue (item partials + correction rows) runs
   // right behind the near field, concurrently with the far field
   record(op, ST_P2P, true, sn);
-  const bool split_epi = !c.dense && (c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE);
+  const bool split_epi = !c.dense && (c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE || c.kind == K_STOKESLET);
   if (split_epi) launch_layer_epilogue(op, c, sharded, sn, 1);
   if (!serial) FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
   // far field on the main stream
