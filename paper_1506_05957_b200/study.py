@@ -19,12 +19,13 @@ import time
 
 import numpy as np
 
+from .fmm import KernelKind, evaluate
 from .meshes import make_octasphere, make_rbc
-from .operator import Formulation, GpuBemOperator
+from .operator import Formulation, GpuBemOperator, GpuFmmPlan
 from .solver import solve
 
 __all__ = ["StudyReport", "observed_order", "richardson", "run_relaxation_comparison",
-           "run_convergence"]
+           "run_convergence", "run_scaling"]
 
 
 def observed_order(f1, f2, f3, c=4.0):
@@ -229,4 +230,33 @@ def run_convergence(problem, levels, p=12, tol=1e-6, theta=0.5, n_crit=126, p_mi
                 pass
         rep.derived["orders"] = orders
         rep.derived["order"] = float(np.mean(orders)) if orders else float("nan")
+    return rep
+
+
+def run_scaling(sizes, p=5, n_crit=126, theta=0.5, repeats=1, seed=0, warmup=1):
+    """Wall time of one Laplace single-layer tree evaluation (far + near field, plan
+    prebuilt) over problem sizes, uniform random points in the unit cube, and the
+    fitted log-log slope (reference `study.py:245-273`; ~1 for linear scaling)."""
+    sizes = [int(n) for n in sizes]
+    rng = np.random.default_rng(seed)
+    rep = StudyReport("scaling", dict(p=p, n_crit=n_crit, theta=theta, repeats=repeats, seed=seed))
+    times = []
+    for n in sizes:
+        pos = rng.uniform(0.0, 1.0, size=(n, 3))
+        q = rng.uniform(-1.0, 1.0, size=n)
+        plan = GpuFmmPlan(pos, pos, n_crit=n_crit, theta=theta)
+        try:
+            for _ in range(max(0, warmup)):
+                evaluate(KernelKind.LAPLACE_SINGLE, pos, q, pos, p=p, plan=plan)
+            ts = []
+            for _ in range(max(1, repeats)):
+                t0 = time.perf_counter()
+                evaluate(KernelKind.LAPLACE_SINGLE, pos, q, pos, p=p, plan=plan)
+                ts.append(time.perf_counter() - t0)
+        finally:
+            plan.close()
+        times.append(float(np.mean(ts)))
+        rep.records.append(dict(N=n, time=times[-1], time_min=float(min(ts)), time_max=float(max(ts))))
+    if len(sizes) >= 2:
+        rep.derived["slope"] = float(np.polyfit(np.log(sizes), np.log(times), 1)[0])
     return rep
