@@ -1,20 +1,20 @@
 #!/usr/bin/env python
-"""Benchmark: FMM mat-vecs/s of relaxed GMRES at N panels (BASELINE.json configs[1] = cfg2).
+"""Benchmark: FMM mat-vecs/s of relaxed GMRES at N panels on BASELINE.json configs[4] (cfg5).
 
-One step = one relaxed-GMRES solve of cfg2 (icosphere L5, 20480 panels, Laplace
-2nd kind, 3 seeded interior charges, theta 0.5, n_crit 128, tol 1e-6, p 12 -> 3,
-unrestarted) with b resident in HBM; value = mat-vecs (applies) done / device
-time, whole job.  ``e2e`` is the same metric through the public Python API
-(``solver.solve`` on a host pinned b, result read back to the host).
+cfg5 is the largest single-GPU configuration of BASELINE.json (and north_star's strong-scaling
+config): icosphere L7, 327 680 panels, Laplace 2nd kind, 8 seeded interior charges, theta 0.5,
+n_crit 256, tol 1e-6, p 14 -> 3, unrestarted.  One step = one relaxed-GMRES solve with b
+resident in HBM; value = mat-vecs (applies) done / device time, whole job.  ``e2e`` is the same
+metric through the public Python API (``solver.solve`` path: host pinned b -> host x).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfgK]
 
-Under torchrun (N > 1) the same solve is partitioned over the N GPUs (strong
-scaling): each rank owns a work-balanced range of target and source leaves,
-leaf multipoles and result slices are exchanged with NCCL all-gathers, GMRES
-runs replicated; device time is the max over ranks.  ``--impl reference``
-times the CPU oracle port of the reference path (oracle/fmm_oracle.py) on the
-host cores, rank 0 only.
+Under torchrun (N > 1) the same solve is partitioned over the N GPUs (strong scaling).
+``--impl reference`` times the reference's CPU path on the host cores: the oracle port
+(oracle/fmm_oracle.py, pinned to the unmodified reference by tests/golden) with its per-leaf /
+per-cell loops spread over every host core (oracle/parallel_oracle.py); one step = one apply,
+cycling the relaxed orders the reference's own solve used on this config (tests/golden), rank 0
+only.
 """
 
 from __future__ import annotations
@@ -34,7 +34,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG_NAME = "cfg2"
+CONFIG_NAME = "cfg5"
 P2P_FLOPS_PER_INTERACTION = {"laplace_second": 18, "laplace_first": 11, "stokes": 29}
 
 
@@ -46,6 +46,7 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=CONFIG_NAME)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-leg", action="store_true", help=argparse.SUPPRESS)  # internal subprocess
     return ap.parse_args()
 
 
@@ -54,72 +55,113 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def workload_desc(cfg, mesh):
+def workload_desc(cfg, mesh, world):
+    """The config dict both arms print (the driver compares them)."""
     return {
-        "workload": f"{cfg.name}: {mesh.n_panels}-panel icosphere, {cfg.formulation}, "
-                    f"{cfg.n_charges} seeded interior charges, theta {cfg.theta}, n_crit {cfg.n_crit}, "
-                    f"relaxed GMRES tol {cfg.tol:g}, p {cfg.p_initial}->{cfg.p_min}, unrestarted",
+        "workload": f"{cfg.name}: {mesh.n_panels}-panel {'RBC lattice' if cfg.name == 'cfg4' else 'icosphere'}, "
+                    f"{cfg.formulation}, "
+                    + (f"{cfg.n_charges} seeded interior charges, " if cfg.n_charges else "")
+                    + f"theta {cfg.theta}, n_crit {cfg.n_crit}, relaxed GMRES tol {cfg.tol:g}, "
+                    f"p {cfg.p_initial}->{cfg.p_min}, unrestarted",
         "panels": mesh.n_panels,
         "unknowns": mesh.n_panels * (3 if cfg.formulation == "stokes" else 1),
         "gauss_points_far": 4,
         "near_rule": "19-pt degree 9 + 32-node polar singular",
         "step": "one relaxed GMRES solve (b resident in HBM)",
         "l2": "256 MiB buffer written between timed steps (L2 flush)",
+        "parallelism": f"shard{world}" if world > 1 else "single",
     }
+
+
+def golden_orders(cfg):
+    """The relaxed orders the UNMODIFIED reference's solve used on this config (tests/golden)."""
+    for f in (f"{cfg.name}.npz", f"{cfg.name}_sampled.npz", f"{cfg.name}_solve.npz"):
+        path = os.path.join(ROOT, "tests", "golden", f)
+        if os.path.exists(path):
+            d = np.load(path)
+            if "relaxed_orders" in d:
+                return [int(v) for v in d["relaxed_orders"]]
+    return [cfg.p_initial]
 
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled DURING the timed region (NVML, every 10 ms, in a
+    thread; the timed region of a cfg5 run is only ~0.2 s)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
-        self.proc = None
-        self.path = None
+        self.sm, self.smax, self.reasons = [], [], set()
+        self._stop = None
+        self._thr = None
+        self.err = None
 
     def __enter__(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except (FileNotFoundError, OSError):
-            self.proc = None
-        time.sleep(0.3)
+            import pynvml
+
+            pynvml.nvmlInit()
+            uuid = None
+            try:
+                import torch
+
+                uuid = str(torch.cuda.get_device_properties(self.gpu).uuid)
+            except Exception:
+                pass
+            h = None
+            if uuid:
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    hi = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    u = pynvml.nvmlDeviceGetUUID(hi)
+                    u = u.decode() if isinstance(u, bytes) else u
+                    if u.replace("GPU-", "") == uuid.replace("GPU-", ""):
+                        h = hi
+            self.h = h if h is not None else pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nv = pynvml
+        except Exception as exc:
+            self.err = f"nvml unavailable: {exc}"
+            return self
+        self._stop = threading.Event()
+
+        def loop():
+            nv = self.nv
+            while not self._stop.is_set():
+                self.sample()
+                self._stop.wait(0.01)
+
+        self.sample()
+        self._thr = threading.Thread(target=loop, daemon=True)
+        self._thr.start()
         return self
 
+    def sample(self):
+        nv = self.nv
+        try:
+            self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+            self.smax.append(float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)))
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for nm, bit in self.REASONS.items():
+                if mask & bit:
+                    self.reasons.add(nm)
+        except Exception as exc:
+            self.err = str(exc)
+
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join(timeout=2)
+            self.sample()
 
     def summary(self):
-        if self.proc is None or not self.path or not os.path.exists(self.path):
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        rows = list(csv.reader(io.StringIO(open(self.path).read())))
-        os.unlink(self.path)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows[1:]:
-            if len(r) < 9:
-                continue
-            try:
-                sm.append(float(r[1].split()[0]))
-                smax.append(float(r[2].split()[0]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, r[5:9]):
-                if v.strip() == "Active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(max(smax)) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"]}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": float(max(self.smax)),
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml 10 ms"}
 
 
 # ---------------------------------------------------------------- CPU (oracle) legs
@@ -133,53 +175,109 @@ def cpu_threads():
     return n
 
 
-def cpu_baseline_sample(cfg, mesh, b):
-    """Oracle port (oracle/fmm_oracle.py): one relaxed GMRES solve of the same config."""
-    from oracle import fmm_oracle as O
+def host_info():
+    """CPU model, core count and the numpy / scipy / BLAS builds the CPU legs run on."""
+    info = {"cpu_model": None, "cores": os.cpu_count()}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    import scipy
 
-    cores = cpu_threads()
-    op = O.OracleOperator(mesh, cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu)
+    info["numpy"] = np.__version__
+    info["scipy"] = scipy.__version__
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["blas"] = [f"{d.get('internal_api')} {d.get('version')} ({d.get('threading_layer')}, "
+                        f"{d.get('num_threads')} threads)" for d in threadpool_info()
+                        if d.get("user_api") == "blas"]
+    except Exception:
+        info["blas"] = None
+    return info
+
+
+def oracle_setup(cfg, mesh, orders, workers):
+    from oracle import fmm_oracle as O
+    from oracle.parallel_oracle import ParallelOracle
+
     t0 = time.perf_counter()
-    r = O.gmres(op.apply, b, O.RelaxationSchedule(cfg.p_initial, cfg.p_min, cfg.tol, True), cfg.tol,
-                cfg.max_iter)
+    op = O.OracleOperator(mesh, cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu)
+    setup_s = time.perf_counter() - t0
+    par = ParallelOracle(op, orders, workers=workers)
+    return op, par, setup_s
+
+
+def cpu_leg_main(args, cfg, mesh):
+    """Subprocess body of the in-arm cpu_baseline (a fork pool must not inherit a CUDA context):
+    one apply at every distinct relaxed order of the reference's solve on this config."""
+    cores = cpu_threads()
+    orders = golden_orders(cfg)
+    op, par, setup_s = oracle_setup(cfg, mesh, orders, cores)
+    x = np.random.default_rng(1).uniform(-1.0, 1.0, op.n)
+    per_p = {}
+    t0 = time.perf_counter()
+    for p in sorted(set(orders), reverse=True):
+        t1 = time.perf_counter()
+        par.apply(x, p)
+        per_p[str(p)] = time.perf_counter() - t1
     dt = time.perf_counter() - t0
-    return {"value": r.n_iterations / dt, "unit": "matvecs/s", "cores": cores, "kind": "port",
-            "sample": f"one relaxed GMRES solve of {cfg.name} ({r.n_iterations} mat-vecs at p "
-                      f"{r.orders}, {dt:.1f} s; setup excluded, as the reference's study.py:196-204)",
-            "time_to_solution_s": dt}
+    par.close()
+    # a relaxed solve's mat-vecs at the reference's own orders, from the per-order times
+    solve_s = sum(per_p[str(p)] for p in orders)
+    print(json.dumps({"value": len(orders) / solve_s, "unit": "matvecs/s", "cores": cores,
+                      "kind": "port",
+                      "sample": f"one apply of {cfg.name} at each order of the reference's relaxed "
+                                f"solve {orders} ({dt:.1f} s of CPU work); value = {len(orders)} "
+                                f"mat-vecs / the sum of their apply times. oracle/fmm_oracle.py "
+                                "restates the reference (pinned by tests/golden); its leaf/cell "
+                                "loops run on every host core (oracle/parallel_oracle.py)",
+                      "apply_s_per_p": per_p, "setup_s": setup_s, "host": host_info()}),
+          flush=True)
+
+
+def cpu_baseline_sample(args, cfg):
+    """Runs cpu_leg_main in a fresh process (bench.py --cpu-leg) and returns its JSON."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-leg", "--config", cfg.name]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=dict(os.environ))
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # the GPU line must still print
+        return {"value": None, "unit": "matvecs/s", "cores": os.cpu_count(), "kind": "port",
+                "sample": f"cpu leg failed: {type(exc).__name__}: {exc}"[:300]}
 
 
 def run_reference(args, cfg, mesh, world):
     rank, _, _ = dist_env()
     if rank != 0:
         return
-    from oracle import fmm_oracle as O
-    from paper_1506_05957_b200.configs import CONFIGS  # noqa: F401
-
     cores = cpu_threads()
-    op = O.OracleOperator(mesh, cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu)
-    data = cfg.boundary_data(op.centroids, op.normals)
+    orders = golden_orders(cfg)
+    op, par, setup_s = oracle_setup(cfg, mesh, orders, cores)
     x = np.random.default_rng(1).uniform(-1.0, 1.0, op.n)
-    # the relaxed schedule the solve follows on this config (pinned by tests/golden/cfg2.npz)
-    schedule = [cfg.p_initial, cfg.p_initial, 10, 5] if cfg.name == "cfg2" else [cfg.p_initial]
-    del data
     for i in range(args.warmup):
-        op.apply(x, schedule[i % len(schedule)])
+        par.apply(x, orders[i % len(orders)])
     t0 = time.perf_counter()
     for i in range(args.steps):
-        op.apply(x, schedule[i % len(schedule)])
+        par.apply(x, orders[i % len(orders)])
     dt = time.perf_counter() - t0
+    par.close()
     value = args.steps / dt
+    sample = (f"{args.steps} applies of {cfg.name} cycling p over {orders} (the orders of the "
+              "reference's own relaxed solve, tests/golden); oracle/fmm_oracle.py restates the "
+              "reference (pinned by tests/golden), its leaf/cell loops on all host cores "
+              "(oracle/parallel_oracle.py); setup excluded like study.py:196-204")
     line = {
         "metric": f"FMM mat-vecs/s at N={mesh.n_panels} panels (relaxed GMRES, {cfg.name})",
         "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_desc(cfg, mesh), "impl": "reference",
+        "config": workload_desc(cfg, mesh, world), "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "matvecs/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} mat-vecs cycling p over {schedule} (the relaxed "
-                                   "schedule); oracle/fmm_oracle.py restates the reference, pinned "
-                                   "by tests/golden"},
+                         "sample": sample, "setup_s": setup_s, "host": host_info()},
         "e2e": {"value": value, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -221,10 +319,16 @@ def run_ours(args, cfg, mesh, world):
         tdist.init_process_group("nccl")
     device = local if dist else 0
     torch.cuda.set_device(device)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter()
     op = GpuBemOperator(mesh, cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu,
                         device=device)
+    setup_s = time.perf_counter() - t_setup  # BemOperator.__init__ (bemop.py:50-82), host->host
     data = cfg.boundary_data(op.centroids, op.normals)
+    op.assemble_rhs(data)  # first call builds the p=18 tables
+    t_rhs = time.perf_counter()
     b_host = op.assemble_rhs(data)
+    rhs_s = time.perf_counter() - t_rhs  # assemble_rhs (bemop.py:290-310), host->host
     if dist:
         from paper_1506_05957_b200.parallel import shard_operator
 
@@ -244,9 +348,10 @@ def run_ours(args, cfg, mesh, world):
 
     def solve_device():
         N.check(lib.fmmbem_op_gmres_device(op._h, ctypes.c_void_p(b_dev.data_ptr()), cfg.tol,
-                                           cfg.p_initial, cfg.p_min, 1, cfg.max_iter,
+                                           cfg.tol, cfg.p_initial, cfg.p_min, 1, cfg.max_iter,
                                            ctypes.c_void_p(x_dev.data_ptr()), N.dptr(res),
-                                           N.i32ptr(ords), ctypes.byref(nit), ctypes.byref(conv)))
+                                           N.i32ptr(ords), ctypes.byref(nit), ctypes.byref(conv),
+                                           None, None, None))
         return int(nit.value), [int(o) for o in ords[:nit.value]]
 
     op.set_timing(False)  # the timed steps run the plain graphs; stages come from a separate pass
@@ -297,7 +402,7 @@ def run_ours(args, cfg, mesh, world):
     op.set_serial(False)
     op.set_timing(False)
     dev_ms = float(np.sum(step_ms))
-    applies = applies1 - applies0
+    applies = sum(len(o) for o in orders_seen)  # mat-vecs done by the timed solves
     from paper_1506_05957_b200.parallel import reduce_timing
 
     # one partitioned job: every rank takes part in the same mat-vecs (strong scaling)
@@ -308,6 +413,8 @@ def run_ours(args, cfg, mesh, world):
     # e2e through the public API: host pinned b -> solve() -> host x
     b_pin = torch.from_numpy(b_host).pin_memory().numpy()
     e2e_ms, e2e_applies, d2h = [], 0, 0
+    for _ in range(args.warmup):  # the first host-API call allocates its pinned staging
+        _device_gmres(op, b_pin, sched, cfg.tol, cfg.max_iter)
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -361,18 +468,39 @@ def run_ours(args, cfg, mesh, world):
             "m2l": {"achieved": algo["m2l"] / (iso["m2l"] * 1e-3) / 1e12,
                     "frac": algo["m2l"] / (iso["m2l"] * 1e-3) / 1e12 / fp64_peak}},
     }
+    # apply(x, p) throughput per order (headline unit): CUDA events around
+    # back-to-back device applies on the op's stream, x resident in HBM
+    xin = torch.from_numpy(np.random.default_rng(1).uniform(-1.0, 1.0, n)).to(f"cuda:{device}")
+    yout = torch.empty_like(xin)
+    per_p = {}
+    if not dist:
+        stream = torch.cuda.current_stream(device)
+        for p in sorted(set(p for o in orders_seen for p in o), reverse=True):
+            for _ in range(2):
+                op.apply_device(xin.data_ptr(), yout.data_ptr(), p, stream=stream.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 10
+            e0.record(stream)
+            for _ in range(reps):
+                op.apply_device(xin.data_ptr(), yout.data_ptr(), p, stream=stream.cuda_stream)
+            e1.record(stream)
+            e1.synchronize()
+            per_p[str(p)] = {"applies_per_s": reps / (e0.elapsed_time(e1) * 1e-3),
+                             "ms": e0.elapsed_time(e1) / reps}
     if rank != 0:
         return
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = cpu_baseline_sample(cfg, mesh, b_host)
+        cpu = cpu_baseline_sample(args, cfg)
     line = {
         "metric": f"FMM mat-vecs/s at N={mesh.n_panels} panels (relaxed GMRES, {cfg.name})",
         "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_desc(cfg, mesh), parallelism=f"shard{world}" if world > 1 else "single"),
+        "config": workload_desc(cfg, mesh, world),
         "time_to_solution_ms": dev_ms_max / args.steps,
+        "setup_s": setup_s, "rhs_s": rhs_s,
+        "apply_per_p": per_p,
         "iterations": len(orders_seen[-1]), "orders": orders_seen[-1],
         "wall_s_timed_region": wall,
         "e2e": {"value": e2e_value, "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n,
@@ -382,6 +510,7 @@ def run_ours(args, cfg, mesh, world):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": int(launches1 - launches0),
+        "matvecs_timed": applies,
         "structure": {"p2p_interactions_per_apply": op.plan.p2p_interactions,
                       "m2l_pairs": op.plan.n_m2l, "src_cells": op.plan.n_src_cells,
                       "tgt_cells": op.plan.n_tgt_cells},
@@ -397,7 +526,9 @@ def main():
     mesh = cfg.mesh()
     _, world, _ = dist_env()
     world = max(world, 1)
-    if args.impl == "reference":
+    if args.cpu_leg:
+        cpu_leg_main(args, cfg, mesh)
+    elif args.impl == "reference":
         run_reference(args, cfg, mesh, world)
     else:
         run_ours(args, cfg, mesh, world)

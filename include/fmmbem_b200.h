@@ -96,8 +96,10 @@ int fmmbem_op_size(const fmmbem_op* op, int64_t* n);
 int fmmbem_op_plan(fmmbem_op* op, fmmbem_plan** plan);
 /* BemOperator.apply(x, p) (bemop.py:272-274), host x (n) -> host y (n) */
 int fmmbem_op_apply(fmmbem_op* op, const double* x, double* y, int p);
-/* same with device pointers, stream-ordered on the op's stream; synchronises
- * before returning.  stream is reserved (pass NULL). */
+/* same with device pointers.  Stream-ordered with the caller: the op's work starts after the
+ * work already queued on `stream` and `stream` waits for it on return.  stream = NULL: after
+ * the legacy default stream (torch's default), and the call synchronises before returning;
+ * a non-NULL stream returns without a host synchronisation (y_dev is ready in `stream` order). */
 int fmmbem_op_apply_device(fmmbem_op* op, const double* x_dev, double* y_dev, int p, void* stream);
 /* BemOperator.dense_apply(x) (bemop.py:276-278) */
 int fmmbem_op_dense_apply(fmmbem_op* op, const double* x, double* y);
@@ -108,17 +110,27 @@ int fmmbem_op_assemble_rhs(fmmbem_op* op, const double* data, int p, int dense, 
  * nnz_pairs and block; indptr (P+1), indices (nnz), data (nnz*block). */
 int fmmbem_op_correction(const fmmbem_op* op, int which, int64_t* nnz_pairs, int32_t* block,
                          int64_t* indptr, int64_t* indices, double* data);
-/* solver.solve / solver.gmres with the relaxation schedule (solver.py:20-143) on
- * the device.  Host b (n) -> host x (n); residuals / orders (max_iter) are filled
- * for the n_iter iterations done. */
-int fmmbem_op_gmres(fmmbem_op* op, const double* b, double tol, int p_initial, int p_min,
-                    int relaxed, int max_iter, double* x, double* residuals, int32_t* orders,
-                    int32_t* n_iter, int32_t* converged);
-/* device-pointer GMRES (b_dev, x_dev on the op's device) */
-int fmmbem_op_gmres_device(fmmbem_op* op, const double* b_dev, double tol, int p_initial,
-                           int p_min, int relaxed, int max_iter, double* x_dev,
+/* Progress callback of the GMRES loop, called after every iteration like the reference's
+ * callback(k, residual, p) (solver.py:122-123); k is 1-based.  Return 0 to continue; a nonzero
+ * return stops the solve after this iteration (the Python binding uses it to re-raise an
+ * exception the callback threw).  May be NULL. */
+typedef int (*fmmbem_gmres_callback)(int32_t k, double residual, int32_t p, void* user);
+/* solver.solve / solver.gmres with the relaxation schedule (solver.py:20-143) on the device.
+ * tol is the stop test (|g_{k+1}|/||b|| < tol, solver.py:119,124); eta drives the order
+ * (RelaxationSchedule.eta, solver.py:41-47; solve() passes eta = tol, solver.py:141-143).
+ * Host b (n) -> host x (n); residuals / orders (max_iter) are filled for the n_iter
+ * iterations done. */
+int fmmbem_op_gmres(fmmbem_op* op, const double* b, double tol, double eta, int p_initial,
+                    int p_min, int relaxed, int max_iter, double* x, double* residuals,
+                    int32_t* orders, int32_t* n_iter, int32_t* converged,
+                    fmmbem_gmres_callback callback, void* user);
+/* device-pointer GMRES (b_dev, x_dev on the op's device), stream-ordered with `stream` like
+ * fmmbem_op_apply_device (NULL = legacy default stream); always returns with x_dev complete. */
+int fmmbem_op_gmres_device(fmmbem_op* op, const double* b_dev, double tol, double eta,
+                           int p_initial, int p_min, int relaxed, int max_iter, double* x_dev,
                            double* residuals, int32_t* orders, int32_t* n_iter,
-                           int32_t* converged);
+                           int32_t* converged, fmmbem_gmres_callback callback, void* user,
+                           void* stream);
 /* instrumentation: enable per-stage CUDA-event timing of every apply (0/1), read
  * the accumulated milliseconds per stage [p2p, p2m+m2m, m2l, l2l, epilogue, total]
  * and the number of timed applies, reset them; use_graphs toggles CUDA graphs. */

@@ -54,12 +54,14 @@ SIGNATURES = {
                                               _c_double_p]),
     "fmmbem_op_correction": (ctypes.c_int, [_vp, ctypes.c_int, _c_int64_p, _c_int32_p, _c_int64_p,
                                             _c_int64_p, _c_double_p]),
-    "fmmbem_op_gmres": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_double, ctypes.c_int,
-                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_double_p,
-                                       _c_double_p, _c_int32_p, _c_int32_p, _c_int32_p]),
-    "fmmbem_op_gmres_device": (ctypes.c_int, [_vp, _vp, ctypes.c_double, ctypes.c_int,
-                                              ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
-                                              _c_double_p, _c_int32_p, _c_int32_p, _c_int32_p]),
+    "fmmbem_op_gmres": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       _c_double_p, _c_double_p, _c_int32_p, _c_int32_p,
+                                       _c_int32_p, _vp, _vp]),
+    "fmmbem_op_gmres_device": (ctypes.c_int, [_vp, _vp, ctypes.c_double, ctypes.c_double,
+                                              ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_int, _vp, _c_double_p, _c_int32_p,
+                                              _c_int32_p, _c_int32_p, _vp, _vp, _vp]),
     "fmmbem_op_set_timing": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int]),
     "fmmbem_op_set_serial": (ctypes.c_int, [_vp, ctypes.c_int]),
     "fmmbem_op_stage_times": (ctypes.c_int, [_vp, _c_double_p, _c_int64_p, ctypes.c_int]),
@@ -70,6 +72,10 @@ SIGNATURES = {
                                        ctypes.c_char_p]),
     "fmmbem_op_unshard": (ctypes.c_int, [_vp]),
 }
+
+# int (*)(int32_t k, double residual, int32_t p, void* user)  (fmmbem_gmres_callback)
+GMRES_CALLBACK = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
+                                  ctypes.c_void_p)
 
 _lib = None
 

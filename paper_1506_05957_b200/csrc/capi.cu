@@ -72,6 +72,19 @@ __global__ void k_dfma_probe(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
+// Stream ordering with the caller (include/fmmbem_b200.h): the op's own stream waits for
+// the work already queued on the caller's stream (NULL = the legacy default stream, where
+// torch queues by default), and the caller's stream waits for the op's work on the way out.
+void enter_caller_stream(BemOp& op, cudaStream_t caller) {
+  FMM_CUDA(cudaEventRecord(op.ev_enter, caller));
+  FMM_CUDA(cudaStreamWaitEvent(op.s_main, op.ev_enter, 0));
+}
+
+void leave_caller_stream(BemOp& op, cudaStream_t caller) {
+  FMM_CUDA(cudaEventRecord(op.ev_leave, op.s_main));
+  FMM_CUDA(cudaStreamWaitEvent(caller, op.ev_leave, 0));
+}
+
 }  // namespace
 
 extern "C" {
@@ -294,14 +307,20 @@ int fmmbem_op_apply(fmmbem_op* h, const double* x, double* y, int p) {
   });
 }
 
-int fmmbem_op_apply_device(fmmbem_op* h, const double* x_dev, double* y_dev, int p, void*) {
+int fmmbem_op_apply_device(fmmbem_op* h, const double* x_dev, double* y_dev, int p, void* stream) {
   return guarded([&] {
     FMM_REQUIRE(h && x_dev && y_dev, "null argument");
     FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p must be in [0, 20]");
     select(h->device);
-    op_apply_device(*h->op, x_dev, y_dev, p);
-    FMM_CUDA(cudaStreamSynchronize(h->op->s_main));
-    op_collect_stage_times(*h->op);
+    BemOp& op = *h->op;
+    const cudaStream_t caller = (cudaStream_t)stream;
+    enter_caller_stream(op, caller);
+    op_apply_device(op, x_dev, y_dev, p);
+    leave_caller_stream(op, caller);
+    if (!caller || op.timing) {  // NULL stream: synchronous, like the host variant
+      FMM_CUDA(cudaStreamSynchronize(op.s_main));
+      op_collect_stage_times(op);
+    }
   });
 }
 
@@ -356,10 +375,12 @@ int fmmbem_op_correction(const fmmbem_op* h, int which, int64_t* nnz_pairs, int3
   });
 }
 
-static void gmres_common(fmmbem_op* h, const double* b_dev, double tol, int p_initial, int p_min,
-                         int relaxed, int max_iter, double* x_dev, double* residuals,
-                         int32_t* orders, int32_t* n_iter, int32_t* converged) {
-  GmresResult r = op_gmres(*h->op, b_dev, tol, p_initial, p_min, relaxed != 0, max_iter, x_dev);
+static void gmres_common(fmmbem_op* h, const double* b_dev, double tol, double eta, int p_initial,
+                         int p_min, int relaxed, int max_iter, double* x_dev, double* residuals,
+                         int32_t* orders, int32_t* n_iter, int32_t* converged,
+                         fmmbem_gmres_callback cb, void* user) {
+  GmresResult r = op_gmres(*h->op, b_dev, tol, eta, p_initial, p_min, relaxed != 0, max_iter,
+                           x_dev, cb, user);
   for (size_t k = 0; k < r.orders.size(); ++k) {
     if (residuals) residuals[k] = r.residuals[k];
     if (orders) orders[k] = r.orders[k];
@@ -368,9 +389,10 @@ static void gmres_common(fmmbem_op* h, const double* b_dev, double tol, int p_in
   if (converged) *converged = r.converged ? 1 : 0;
 }
 
-int fmmbem_op_gmres(fmmbem_op* h, const double* b, double tol, int p_initial, int p_min,
-                    int relaxed, int max_iter, double* x, double* residuals, int32_t* orders,
-                    int32_t* n_iter, int32_t* converged) {
+int fmmbem_op_gmres(fmmbem_op* h, const double* b, double tol, double eta, int p_initial,
+                    int p_min, int relaxed, int max_iter, double* x, double* residuals,
+                    int32_t* orders, int32_t* n_iter, int32_t* converged,
+                    fmmbem_gmres_callback cb, void* user) {
   return guarded([&] {
     FMM_REQUIRE(h && b && x, "null argument");
     select(h->device);
@@ -379,8 +401,8 @@ int fmmbem_op_gmres(fmmbem_op* h, const double* b, double tol, int p_initial, in
     op.stage_y.ensure(op.n);
     FMM_CUDA(cudaEventRecord(op.call_ev[0], op.s_main));
     FMM_CUDA(cudaMemcpyAsync(op.stage_x.get(), b, op.n * sizeof(double), cudaMemcpyHostToDevice, op.s_main));
-    gmres_common(h, op.stage_x.get(), tol, p_initial, p_min, relaxed, max_iter, op.stage_y.get(),
-                 residuals, orders, n_iter, converged);
+    gmres_common(h, op.stage_x.get(), tol, eta, p_initial, p_min, relaxed, max_iter,
+                 op.stage_y.get(), residuals, orders, n_iter, converged, cb, user);
     // x through a pinned staging buffer (a pageable D2H copy is staged by the driver, slower)
     if (op.xpin_cap < op.n) {
       if (op.xpin_h) FMM_CUDA(cudaFreeHost(op.xpin_h));
@@ -398,17 +420,22 @@ int fmmbem_op_gmres(fmmbem_op* h, const double* b, double tol, int p_initial, in
   });
 }
 
-int fmmbem_op_gmres_device(fmmbem_op* h, const double* b_dev, double tol, int p_initial,
-                           int p_min, int relaxed, int max_iter, double* x_dev, double* residuals,
-                           int32_t* orders, int32_t* n_iter, int32_t* converged) {
+int fmmbem_op_gmres_device(fmmbem_op* h, const double* b_dev, double tol, double eta,
+                           int p_initial, int p_min, int relaxed, int max_iter, double* x_dev,
+                           double* residuals, int32_t* orders, int32_t* n_iter,
+                           int32_t* converged, fmmbem_gmres_callback cb, void* user,
+                           void* stream) {
   return guarded([&] {
     FMM_REQUIRE(h && b_dev && x_dev, "null argument");
     select(h->device);
     BemOp& op = *h->op;
+    const cudaStream_t caller = (cudaStream_t)stream;
+    enter_caller_stream(op, caller);
     FMM_CUDA(cudaEventRecord(op.call_ev[0], op.s_main));
-    gmres_common(h, b_dev, tol, p_initial, p_min, relaxed, max_iter, x_dev, residuals, orders,
-                 n_iter, converged);
+    gmres_common(h, b_dev, tol, eta, p_initial, p_min, relaxed, max_iter, x_dev, residuals,
+                 orders, n_iter, converged, cb, user);
     FMM_CUDA(cudaEventRecord(op.call_ev[1], op.s_main));
+    leave_caller_stream(op, caller);
     FMM_CUDA(cudaStreamSynchronize(op.s_main));
     float ms = 0.f;
     FMM_CUDA(cudaEventElapsedTime(&ms, op.call_ev[0], op.call_ev[1]));

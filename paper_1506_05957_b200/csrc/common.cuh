@@ -69,6 +69,23 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   FMM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
+// Per-device one-time setup (constant-memory tables, kernel attributes): both belong to the
+// CURRENT device, so a process that drives several devices must redo them on each one.
+//   static DeviceOnce once;  if (once.first()) { ...; once.mark(); }
+struct DeviceOnce {
+  unsigned long long mask = 0;  // bit d: done on device d
+  bool first() const {
+    int dev = 0;
+    FMM_CUDA(cudaGetDevice(&dev));
+    return !(__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & (1ull << (dev & 63)));
+  }
+  void mark() {
+    int dev = 0;
+    FMM_CUDA(cudaGetDevice(&dev));
+    __atomic_fetch_or(&mask, 1ull << (dev & 63), __ATOMIC_RELEASE);
+  }
+};
+
 #define FMM_REQUIRE(cond, msg)                  \
   do {                                          \
     if (!(cond)) throw ::fmmbem::ArgumentError(msg); \

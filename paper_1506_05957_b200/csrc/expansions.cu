@@ -17,8 +17,8 @@ __constant__ short c_n_of[hcount(P_MAX)];
 __constant__ short c_m_of[hcount(P_MAX)];
 
 void upload_index_tables() {
-  static bool done = false;
-  if (done) return;
+  static DeviceOnce done;
+  if (!done.first()) return;
   short n_of[hcount(P_MAX)], m_of[hcount(P_MAX)];
   for (int n = 0; n <= P_MAX; ++n)
     for (int m = 0; m <= n; ++m) {
@@ -27,7 +27,7 @@ void upload_index_tables() {
     }
   FMM_CUDA(cudaMemcpyToSymbol(c_n_of, n_of, sizeof(n_of)));
   FMM_CUDA(cudaMemcpyToSymbol(c_m_of, m_of, sizeof(m_of)));
-  done = true;
+  done.mark();
 }
 
 // ------------------------------------------------------------------ P2M
@@ -134,11 +134,11 @@ void launch_p2m_t(const TreeDev& S, const int* leaves, int n_leaves, int p, cons
   const int H = hcount(p);
   const int G = P2M_THREADS / H;
   const size_t smem = (size_t)std::max(P2M_CHUNK * H, G * C * H) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (attr.first()) {
     FMM_CUDA(cudaFuncSetAttribute(k_p2m<C, HQ, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(P2M_CHUNK * hcount(P_MAX) * sizeof(double2))));
-    attr = true;
+    attr.mark();
   }
   if (n_leaves) k_p2m<C, HQ, HD><<<n_leaves, P2M_THREADS, smem, st>>>(S, leaves, p, q, d, M);
   FMM_LAUNCH_CHECK();

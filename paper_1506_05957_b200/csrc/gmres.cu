@@ -355,9 +355,10 @@ int schedule_p(double r, double eta, int p_initial, int p_min) {
 
 }  // namespace
 
-GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int p_min,
-                     bool relaxed, int max_iter, double* x) {
-  FMM_REQUIRE(tol > 0.0, "eta must be positive");
+GmresResult op_gmres(BemOp& op, const double* b, double tol, double eta, int p_initial, int p_min,
+                     bool relaxed, int max_iter, double* x, GmresCallback cb, void* user) {
+  // eta drives the order (RelaxationSchedule.order, solver.py:41-47), tol the stop test (:124)
+  FMM_REQUIRE(eta > 0.0, "eta must be positive");
   FMM_REQUIRE(max_iter >= 0, "max_iter must be >= 0");
   FMM_REQUIRE(p_initial >= 0 && p_initial <= P_MAX, "p_initial must be in [0, 20]");
   FMM_REQUIRE(!(op.shard.active && op.shard.virtual_mode),
@@ -456,7 +457,7 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
   int prev_p = p_initial;
   double* hd = scal.get();  // H column k on device: hd[0..k+1]
   for (int k = 0; k < max_iter; ++k) {
-    int p = relaxed ? std::min(schedule_p(residual, tol, p_initial, p_min), prev_p) : p_initial;
+    int p = relaxed ? std::min(schedule_p(residual, eta, p_initial, p_min), prev_p) : p_initial;
     prev_p = p;
     double* w = V.get() + (size_t)(k + 1) * n;
     op_apply_device(op, nullptr, nullptr, p);  // x_in holds v_k (k_scale / k_arnoldi)
@@ -515,6 +516,10 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, int p_initial, int 
     residual = std::fabs(g[k + 1]) / norm_b;
     res.residuals.push_back(residual);
     res.orders.push_back(p);
+    if (cb && cb(k + 1, residual, p, user) != 0) {  // the caller asked to stop (e.g. it raised)
+      res.stopped = true;
+      break;
+    }
     if (residual < tol) {
       res.converged = true;
       break;

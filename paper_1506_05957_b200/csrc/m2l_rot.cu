@@ -429,11 +429,11 @@ void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_
                   const double2* M, double2* pout, cudaStream_t st, bool cls) {
   constexpr int H = hcount(P);
   const size_t smem = (size_t)ROT_WARPS * (16 * H + 4 * P + 4) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (attr.first()) {
     FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
+    attr.mark();
   }
   const int64_t units = (int64_t)n_items * C;
   auto kern = cls ? k_m2l_rot<P, true> : k_m2l_rot<P, false>;

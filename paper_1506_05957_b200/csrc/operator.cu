@@ -19,8 +19,8 @@ namespace fmmbem {
 void upload_index_tables();
 
 void upload_l2p_constants() {
-  static bool done = false;
-  if (done) return;
+  static DeviceOnce done;
+  if (!done.first()) return;
   static L2PConst h;
   h.diag[0] = 1.0;
   for (int m = 1; m <= P_MAX; ++m) h.diag[m] = h.diag[m - 1] * (-1.0 / (2.0 * m));
@@ -31,7 +31,7 @@ void upload_l2p_constants() {
       h.rb[n * (P_MAX + 1) + m] = (n >= m + 2) ? 1.0 / d : 0.0;
     }
   FMM_CUDA(cudaMemcpyToSymbol(c_l2p, &h, sizeof(h)));
-  done = true;
+  done.mark();
 }
 
 namespace {
@@ -425,6 +425,8 @@ BemOp::~BemOp() {
     if (e) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_enter) cudaEventDestroy(ev_enter);
+  if (ev_leave) cudaEventDestroy(ev_leave);
   if (s_main) cudaStreamDestroy(s_main);
   if (s_near) cudaStreamDestroy(s_near);
 }
@@ -454,6 +456,8 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   FMM_CUDA(cudaStreamCreateWithPriority(&op.s_near, cudaStreamNonBlocking, near_hi ? prio_hi : prio_lo));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_join, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&op.ev_enter, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&op.ev_leave, cudaEventDisableTiming));
   for (auto& e : op.ev) FMM_CUDA(cudaEventCreate(&e));
   for (auto& e : op.call_ev) FMM_CUDA(cudaEventCreate(&e));
   cudaStream_t s = op.s_main;
@@ -692,7 +696,14 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
                                           op.x_in.get(), op.y_out.get(), op.m2l_part.get(),
                                           op.p2m_basis.get(), op.m2m_cout.get(), op.plan.rotf.get(),
                                           op.plan.rot_aux.get(), op.plan.rot_dir.get(), op.cl_panel.get(),
-                                          op.p2m_items.d.get(), op.p2m_reduce.d.get(), op.p2m_part.get()};
+                                          op.p2m_items.d.get(), op.p2m_reduce.d.get(), op.p2m_part.get(),
+                                          // table LAYOUTS baked into the captured kernel arguments
+                                          // (a regrown table may come back at the same address)
+                                          (const void*)(intptr_t)op.plan.rot_p,
+                                          (const void*)(intptr_t)op.plan.igrid_p,
+                                          (const void*)(intptr_t)op.basis_p,
+                                          (const void*)(intptr_t)op.plan.n_rot_dirs,
+                                          (const void*)(intptr_t)op.basis_cols};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;

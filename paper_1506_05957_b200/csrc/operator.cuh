@@ -75,6 +75,7 @@ struct BemOp {
   Plan plan;
   cudaStream_t s_main = nullptr, s_near = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_enter = nullptr, ev_leave = nullptr;  // caller-stream ordering (capi.cu)
 
   // geometry, panel order
   DevBuf<double> centroid, normal, area, panel_verts, gauss_pos, gauss_w, fine_pos, fine_w;
@@ -198,6 +199,7 @@ struct GmresResult {
   std::vector<double> residuals;
   std::vector<int> orders;
   bool converged = false;
+  bool stopped = false;  // the progress callback asked to stop
 };
 // sharding (shard.cu)
 void op_shard_setup(BemOp& op, int rank, int world, const int* tleaf_bounds,
@@ -208,8 +210,11 @@ void shard_exchange_multipoles(BemOp& op, int C, int p, cudaStream_t s);
 void shard_exchange_y(BemOp& op, int nc, double* y, cudaStream_t s);
 void nccl_unique_id(unsigned char* out);
 
-GmresResult op_gmres(BemOp& op, const double* b_dev, double tol, int p_initial, int p_min,
-                     bool relaxed, int max_iter, double* x_dev);
+// per-iteration progress (solver.py:122-123): k (1-based), residual, p; nonzero return stops
+typedef int (*GmresCallback)(int32_t k, double residual, int32_t p, void* user);
+GmresResult op_gmres(BemOp& op, const double* b_dev, double tol, double eta, int p_initial,
+                     int p_min, bool relaxed, int max_iter, double* x_dev,
+                     GmresCallback cb = nullptr, void* user = nullptr);
 
 // FmmPlan.far_field / near_field (generic channels, host-facing helper)
 void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig, int p,

@@ -288,11 +288,11 @@ size_t tr_smem() {
 template <int P, int CK, int MODE>
 void tr_launch_one(int nblocks, const TrArgs& a, cudaStream_t st) {
   const size_t sm = tr_smem<P, CK, MODE>();
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (attr.first()) {
     FMM_CUDA(cudaFuncSetAttribute(k_translate<P, CK, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sm));
-    attr = true;
+    attr.mark();
   }
   k_translate<P, CK, MODE><<<nblocks, TrCfg<MODE>::WARPS * 32, sm, st>>>(a);
 }
@@ -545,33 +545,33 @@ void m2lg_launch(const Plan& plan, const int4* gitems, const int* gpair, int n, 
   for (int cb = 0; cb < C;) {
     const int rem = C - cb;
     if (rem >= 4) {
-      static bool a4 = false;
-      if (!a4) {
+      static DeviceOnce a4;
+      if (a4.first()) {
         FMM_CUDA(cudaFuncSetAttribute(k_m2l_grouped<P, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)m2lg_smem<P, 4>()));
-        a4 = true;
+        a4.mark();
       }
       k_m2l_grouped<P, 4><<<n, TR_WARPS * 32, m2lg_smem<P, 4>(), st>>>(
           gitems, gpair, plan.m2l_src.get(), plan.igrid.get(), stride,
           M, C, cb, pout);
       cb += 4;
     } else if (rem >= 2) {
-      static bool a2 = false;
-      if (!a2) {
+      static DeviceOnce a2;
+      if (a2.first()) {
         FMM_CUDA(cudaFuncSetAttribute(k_m2l_grouped<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)m2lg_smem<P, 2>()));
-        a2 = true;
+        a2.mark();
       }
       k_m2l_grouped<P, 2><<<n, TR_WARPS * 32, m2lg_smem<P, 2>(), st>>>(
           gitems, gpair, plan.m2l_src.get(), plan.igrid.get(), stride,
           M, C, cb, pout);
       cb += 2;
     } else {
-      static bool a1 = false;
-      if (!a1) {
+      static DeviceOnce a1;
+      if (a1.first()) {
         FMM_CUDA(cudaFuncSetAttribute(k_m2l_grouped<P, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)m2lg_smem<P, 1>()));
-        a1 = true;
+        a1.mark();
       }
       k_m2l_grouped<P, 1><<<n, TR_WARPS * 32, m2lg_smem<P, 1>(), st>>>(
           gitems, gpair, plan.m2l_src.get(), plan.igrid.get(), stride,
@@ -768,11 +768,11 @@ size_t m2mg_smem() {
 template <int P, int CK>
 void m2mg_launch_one(const int4* items, int n, const int* gchild, const double2* rfull,
                      const double2* M, int C, int cb, double2* cout, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (attr.first()) {
     FMM_CUDA(cudaFuncSetAttribute(k_m2m_grouped<P, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)m2mg_smem<P, CK>()));
-    attr = true;
+    attr.mark();
   }
   k_m2m_grouped<P, CK><<<n, M2M_WARPS * 32, m2mg_smem<P, CK>(), st>>>(items, gchild, rfull, tab_size(P_MAX),
                                                                      M, C, cb, cout);

@@ -289,10 +289,16 @@ class GpuBemOperator:
         N.check(self._lib.fmmbem_op_apply(self._h, N.dptr(v), N.dptr(y), int(p)))
         return y
 
-    def apply_device(self, x_ptr: int, y_ptr: int, p: int = 12):
-        """Device-pointer mat-vec (raw CUDA addresses of n float64 each)."""
+    def apply_device(self, x_ptr: int, y_ptr: int, p: int = 12, stream: int | None = None):
+        """Device-pointer mat-vec (raw CUDA addresses of n float64 each).
+
+        ``stream`` (a raw cudaStream_t, e.g. ``torch.cuda.current_stream().cuda_stream``):
+        the apply is ordered after the work queued there and the stream waits for it; the call
+        returns without a host synchronisation.  ``None``: ordered after the legacy default
+        stream, synchronous."""
         N.check(self._lib.fmmbem_op_apply_device(self._h, ctypes.c_void_p(x_ptr),
-                                                 ctypes.c_void_p(y_ptr), int(p), None))
+                                                 ctypes.c_void_p(y_ptr), int(p),
+                                                 None if stream is None else ctypes.c_void_p(stream)))
 
     def dense_apply(self, x):
         """Direct-sum mat-vec (bemop.py:276-278)."""

@@ -143,3 +143,22 @@ def test_harmonics_addition_theorem():
     Ir = O.solid_harmonics(x, p, irregular=True)
     approx = np.real(np.sum(R * np.conj(Ir), axis=1))
     np.testing.assert_allclose(approx, 1.0 / np.linalg.norm(x - y, axis=1), rtol=1e-12)
+
+
+@pytest.mark.parametrize("name,ps", [("cfg1", [3, 10]), ("stokes_ico3", [5, 9])])
+def test_parallel_oracle_equals_serial_oracle(name, ps):
+    """oracle/parallel_oracle.py (the CPU timing legs) computes the oracle's apply item for item."""
+    from oracle import fmm_oracle as O
+    from oracle.parallel_oracle import ParallelOracle
+    from paper_1506_05957_b200.configs import CONFIGS
+
+    cfg = CONFIGS[name]
+    op = O.OracleOperator(cfg.mesh(), cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu)
+    par = ParallelOracle(op, ps, workers=2)
+    try:
+        x = np.random.default_rng(1).uniform(-1.0, 1.0, op.n)
+        for p in ps:
+            y0, y1 = op.apply(x, p), par.apply(x, p)
+            assert np.linalg.norm(y1 - y0) <= 1e-13 * np.linalg.norm(y0), p
+    finally:
+        par.close()
