@@ -624,8 +624,11 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     const int nlv = own_only ? sw.n_p2m_leaves : pl.src.n_leaves;
     const bool basis = c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p;
     if (basis && op.basis_clustered && !own_only) {
-      // every multipole straight from the sources (no M2M levels)
+      // every multipole straight from the sources (no M2M levels), or the leaves' multipoles
+      // and the M2M chain above them
       launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, nullptr, 0);
+      if (op.basis_leaf_only)
+        launch_m2m_grouped(pl, c.p, C, pl.rshift_src.get(), op.M.get(), op.m2m_cout.get(), s);
     } else {
       if (basis)
         launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, lv, nlv);

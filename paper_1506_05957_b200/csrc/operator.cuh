@@ -117,6 +117,10 @@ struct BemOp {
   // Laplace kinds: the Gauss points of one panel inside one leaf share x[panel],
   // so their basis columns are pre-summed per (leaf, panel) cluster
   bool basis_clustered = false;
+  // clustered kinds: entries for the leaves only, the upper multipoles by octant-grouped M2M
+  // (chosen when the direct table, one entry per (cell, cluster of its subtree), would stream
+  // several times the leaf table's bytes: deep trees such as cfg5)
+  bool basis_leaf_only = false;
   int basis_cols = 0;            // columns of p2m_basis (clusters or sources)
   // direct upward pass (clustered kinds): basis entries (cell, cluster of its subtree)
   // for every M2L source cell and leaf, so the multipoles need no M2M

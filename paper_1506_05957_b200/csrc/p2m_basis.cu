@@ -121,6 +121,9 @@ k_p2m_basis(const int* __restrict__ leaves, const int* __restrict__ body_start,
 // per lane, every row load a coalesced 512 B), the warps' sums are added in
 // warp order through shared memory.
 constexpr int P2M_CHUNK = 64;
+// direct upward pass only while it streams at most this many times the leaf table
+// (cfg2: 3.1x, direct measured faster; cfg5: see DESIGN.md section 4)
+constexpr double UPWARD_DIRECT_MAX_RATIO = 3.5;
 
 template <int NJ>
 __global__ void __launch_bounds__(128)
@@ -302,6 +305,28 @@ bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s) {
     for (int c : pl.h_m2l_src) need[c] = 1;
     for (int c = 0; c < S.n_cells; ++c)
       if (S.h_n_child[c] == 0) need[c] = 1;
+    // entries of the direct table vs the leaf table: the direct pass streams every cluster once
+    // per needed ancestor.  FMMBEM_UPWARD=direct|leaf overrides the choice.
+    {
+      auto count = [&](int c) {
+        const int b0 = S.h_body_start[c], b1 = b0 + S.h_body_count[c];
+        return (int64_t)(std::lower_bound(src_begin.begin(), src_begin.end(), b1) -
+                         std::lower_bound(src_begin.begin(), src_begin.end(), b0));
+      };
+      int64_t e_direct = 0, e_leaf = 0;
+      for (int c = 0; c < S.n_cells; ++c) {
+        if (!need[c]) continue;
+        const int64_t k = count(c);
+        e_direct += k;
+        if (S.h_n_child[c] == 0) e_leaf += k;
+      }
+      const char* env = std::getenv("FMMBEM_UPWARD");
+      const bool leaf = env ? std::string(env) == "leaf"
+                            : (double)e_direct > UPWARD_DIRECT_MAX_RATIO * (double)e_leaf;
+      op.basis_leaf_only = leaf;
+      if (leaf)
+        for (int c = 0; c < S.n_cells; ++c) need[c] = S.h_n_child[c] == 0;
+    }
     std::vector<int> cells, e_cell, e_cl, e_panel, range(2 * (size_t)S.n_cells, 0);
     for (int c = 0; c < S.n_cells; ++c) {
       if (!need[c]) continue;
