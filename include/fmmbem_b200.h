@@ -74,6 +74,23 @@ int fmmbem_plan_pairs(const fmmbem_plan* plan, int which, int32_t* pairs);
 int fmmbem_plan_evaluate(fmmbem_plan* plan, const double* charges, const double* dipoles, int C,
                          int p, int want_gradient, int parts, double* pot, double* grad);
 
+/* ---------------------------------------------------------------- single expansions
+ * The reference's one-expansion API (fmm.py:36-81: Expansion, p2m, m2m, m2l, l2l, m2p, l2p
+ * over harmonics.py:201-270), on the device.  Coefficients use the reference's FULL flat
+ * layout idx(n, m) = n^2 + n + m, complex128 as interleaved (re, im): coeffs (C, (p+1)^2).
+ * Host buffers; `device` selects the GPU.
+ *   p2m:       rel (N,3) = source - center; charges (C,N) and/or dipoles (C,N,3) (NULL = absent)
+ *   translate: kind 0 = m2m (d = old center - new center, fmm.py:56-59),
+ *              1 = m2l (d = target center - source center, :62-65), 2 = l2l (d = new - old, :68-71)
+ *   evaluate:  kind 0 = m2p (multipole_to_point), 1 = l2p (local_to_point); rel (N,3) = target -
+ *              center; pot (C,N), grad (C,N,3) or NULL */
+int fmmbem_expansion_p2m(const double* rel, int64_t n, const double* charges, const double* dipoles,
+                         int C, int p, double* coeffs, int device);
+int fmmbem_expansion_translate(int kind, const double* d, int C, int p, const double* coeffs_in,
+                               double* coeffs_out, int device);
+int fmmbem_expansion_evaluate(int kind, const double* coeffs, int C, int p, const double* rel,
+                              int64_t n, int want_gradient, double* pot, double* grad, int device);
+
 /* ---------------------------------------------------------------- BemOperator
  * Replaces bemop.BemOperator.__init__ (bemop.py:50-82): geometry comes from the
  * host (quadrature.quadrature_points / panel_geometry, quadrature.py:86-121, so

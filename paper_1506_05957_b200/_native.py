@@ -38,6 +38,15 @@ SIGNATURES = {
     "fmmbem_plan_evaluate": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             _c_double_p, _c_double_p]),
+    "fmmbem_expansion_p2m": (ctypes.c_int, [_c_double_p, ctypes.c_int64, _c_double_p, _c_double_p,
+                                            ctypes.c_int, ctypes.c_int, _c_double_p, ctypes.c_int]),
+    "fmmbem_expansion_translate": (ctypes.c_int, [ctypes.c_int, _c_double_p, ctypes.c_int,
+                                                  ctypes.c_int, _c_double_p, _c_double_p,
+                                                  ctypes.c_int]),
+    "fmmbem_expansion_evaluate": (ctypes.c_int, [ctypes.c_int, _c_double_p, ctypes.c_int,
+                                                 ctypes.c_int, _c_double_p, ctypes.c_int64,
+                                                 ctypes.c_int, _c_double_p, _c_double_p,
+                                                 ctypes.c_int]),
     "fmmbem_op_create": (ctypes.c_int, [_c_double_p, ctypes.c_int64, _c_double_p, _c_double_p,
                                         _c_double_p, _c_double_p, _c_double_p, _c_double_p,
                                         _c_double_p, _c_double_p, ctypes.c_int, ctypes.c_int,

@@ -93,6 +93,34 @@ const char* fmmbem_last_error(void) { return g_err.c_str(); }
 
 int fmmbem_version(void) { return 1; }
 
+int fmmbem_expansion_p2m(const double* rel, int64_t n, const double* charges, const double* dipoles,
+                         int C, int p, double* coeffs, int device) {
+  return guarded([&] {
+    FMM_REQUIRE(coeffs && (rel || n == 0), "null argument");
+    select(device);
+    expansion_p2m(rel, n, charges, dipoles, C, p, coeffs, 0);
+  });
+}
+
+int fmmbem_expansion_translate(int kind, const double* d, int C, int p, const double* coeffs_in,
+                               double* coeffs_out, int device) {
+  return guarded([&] {
+    FMM_REQUIRE(d && coeffs_in && coeffs_out, "null argument");
+    select(device);
+    expansion_translate(kind, d, C, p, coeffs_in, coeffs_out, 0);
+  });
+}
+
+int fmmbem_expansion_evaluate(int kind, const double* coeffs, int C, int p, const double* rel,
+                              int64_t n, int want_gradient, double* pot, double* grad, int device) {
+  return guarded([&] {
+    FMM_REQUIRE(coeffs && pot && (rel || n == 0) && (!want_gradient || grad), "null argument");
+    FMM_REQUIRE(C >= 1 && n >= 0, "bad sizes");
+    select(device);
+    expansion_evaluate(kind, coeffs, C, p, rel, n, want_gradient != 0, pot, grad, 0);
+  });
+}
+
 int fmmbem_device_count(int* count) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {

@@ -220,6 +220,14 @@ GmresResult op_gmres(BemOp& op, const double* b_dev, double tol, double eta, int
                      int p_min, bool relaxed, int max_iter, double* x_dev,
                      GmresCallback cb = nullptr, void* user = nullptr);
 
+// single-expansion API (expansion_api.cu, fmm.py:36-81); host buffers, full flat layout
+void expansion_p2m(const double* rel, int64_t N, const double* q, const double* d, int C, int p,
+                   double* coeffs, cudaStream_t s);
+void expansion_translate(int kind, const double* dvec, int C, int p, const double* in, double* out,
+                         cudaStream_t s);
+void expansion_evaluate(int kind, const double* coeffs, int C, int p, const double* rel, int64_t N,
+                        bool want_grad, double* pot, double* grad, cudaStream_t s);
+
 // FmmPlan.far_field / near_field (generic channels, host-facing helper)
 void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig, int p,
                    bool want_grad, int parts, double* pot, double* grad, cudaStream_t s);

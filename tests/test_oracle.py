@@ -162,3 +162,20 @@ def test_parallel_oracle_equals_serial_oracle(name, ps):
             assert np.linalg.norm(y1 - y0) <= 1e-13 * np.linalg.norm(y0), p
     finally:
         par.close()
+
+
+def test_expansion_goldens_are_consistent_with_the_oracle_harmonics():
+    """tests/golden/expansion.npz (reference single-expansion API) vs the oracle's restated
+    harmonics: P2M = q @ R, dipole P2M via the gradient shift rules, M2M via _mat_rconv."""
+    from conftest import load_golden
+
+    g = load_golden("expansion")
+    src, q, nrm = g["src"], g["q"], g["nrm"]
+    for p in (0, 3, 8, 14):
+        R = O.solid_harmonics(src, p)
+        assert np.allclose(q @ R, g[f"p2m_q_p{p}"], rtol=0, atol=1e-13)
+        gx, gy, gz = O.regular_grad(R, p)
+        d = q[:, None] * nrm
+        assert np.allclose(d[:, 0] @ gx + d[:, 1] @ gy + d[:, 2] @ gz, g[f"p2m_d_p{p}"], atol=1e-13)
+        T = O._mat_rconv(O.solid_harmonics(np.array([[-0.3, 0.2, -0.1]]), p)[0], p, "m2m")
+        assert np.allclose(g[f"p2m_q_p{p}"] @ T.T, g[f"m2m_p{p}"], atol=1e-13)
