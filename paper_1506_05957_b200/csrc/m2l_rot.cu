@@ -19,6 +19,7 @@
 // (offset, <= 8 pairs) stages them in shared memory and runs the three stages
 // for up to 8 vectors (pairs x channels) at once; results go to the per-pair
 // slots that k_m2l_gather adds per target cell in a fixed order.
+#include <map>
 #include <utility>
 
 #include "kernels.cuh"
@@ -456,6 +457,267 @@ void launch_rot_dispatch(std::integer_sequence<int, Ps...>, int p, const Plan& p
   FMM_REQUIRE(done, "rotation M2L order out of range");
 }
 
+
+// ---- M2M by rotation --------------------------------------------------------------------
+// The reference's M2M (harmonics.py:156-177, fmm.py:268-290)
+//     M'_n^m = sum_{j<=n, k} M_j^k R_{n-j}^{m-k}(d),   d = c_child - c_parent
+// factors like the M2L: rotate d onto +z (A = a E, the same tables), translate along z, where
+// R_l^mu(|d| z) = |d|^l / l! delta_{mu 0} leaves, per order k, the lower-triangular Toeplitz
+//     M''_n^k = sum_{j=k..n} |d|^{n-j} / (n-j)! M'_j^k,
+// and rotate back with A^{-1} = E^{-1} a~, a~_{mk} = (-1)^{m-k} a_{mk} (the Wigner small-d
+// symmetry d_{km} = (-1)^{k-m} d_{mk}).  In the real split a~ is a with a checkerboard sign, so
+// the back rotation reuses the stage-A fragments with (-1)^k on the input, (-1)^m on the output
+// and the phase e^{+im phi}.  M2M is exact in the reference too, so this agrees with the dense
+// operator to roundoff.
+// per rtab id: e^{-ik phi} (k <= P) and t_l = |d|^l / l! (l <= P)
+__global__ void k_m2m_aux(const double* __restrict__ geo, int n_off, int P, double* __restrict__ aux) {
+  const int stride = aux_stride(P);
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)n_off * stride) return;
+  const int u = (int)(gid / stride), i = (int)(gid % stride);
+  const double r = geo[3 * u], phi = geo[3 * u + 2];
+  double v = 0.0;
+  if (i < 2 * (P + 1)) {
+    double sn, cs;
+    sincos(-(double)(i >> 1) * phi, &sn, &cs);
+    v = (i & 1) ? sn : cs;
+  } else if (i - 2 * (P + 1) <= P) {
+    const int l = i - 2 * (P + 1);
+    double f = 1.0;
+    for (int t = 1; t <= l; ++t) f *= r / t;
+    v = f;
+  }
+  aux[gid] = v;
+}
+
+// warp unit = (item, octet of vectors); vector v of an item = (child v / C, channel v % C);
+// the item's children share one rtab id (level, octant): one direction, phase and |d|
+template <int P>
+__global__ void __launch_bounds__(ROT_WARPS * 32)
+k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ child,
+          const double* __restrict__ frag, const int* __restrict__ dir, int ttot,
+          const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
+          double2* __restrict__ cout) {
+  constexpr int H = hcount(P);
+  constexpr int WS = 16 * H + 4 * P + 4;
+  extern __shared__ double sh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * ROT_WARPS + warp;
+  const int item = unit / C, oct = unit % C;
+  if (item >= n_items) return;
+  const int4 it = items[item];
+  const int nvec = (it.z - it.y) * C, v0 = oct * 8;
+  if (v0 >= nvec) return;
+  double* bre = sh + (size_t)warp * WS;                    // [H][8] real parts
+  double* bim = bre + 8 * H;                               // [H][8] imaginary parts
+  double2* ph = reinterpret_cast<double2*>(bim + 8 * H);   // [P+1] e^{-ik phi}
+  double* tt = reinterpret_cast<double*>(ph + P + 1);      // [P+1] |d|^l / l!
+  const int u = it.x;
+  {
+    const double* A = aux + (size_t)u * aux_stride(aux_p);
+    double* sp = reinterpret_cast<double*>(ph);
+#pragma unroll
+    for (int i = lane; i < 2 * (P + 1); i += 32) sp[i] = A[i];
+#pragma unroll
+    for (int i = lane; i <= P; i += 32) tt[i] = A[2 * (aux_p + 1) + i];
+  }
+  const int fr = lane >> 2, fc = lane & 3;
+  const double* T = frag + (size_t)dir[u] * 4 * ttot * 32 + lane;
+  auto load = [&](Frag& f, int n) {  // stage-A tables (SA_re, SA_im) of degree n
+    const int mt = frag_mt(n), ks = frag_ks(n);
+    const double* tr = T + (size_t)frag_base(n) * 32;
+    const double* ti = tr + (size_t)ttot * 32;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int t = 0; t < FRAG_KS_MAX; ++t)
+        if (q < mt && t < ks) {
+          f.r[q][t] = __ldg(tr + (q * ks + t) * 32);
+          f.i[q][t] = __ldg(ti + (q * ks + t) * 32);
+        }
+  };
+  const double2* msrc = nullptr;
+  {
+    const int vg = v0 + fr;
+    if (vg < nvec) msrc = M + ((size_t)child[it.y + vg / C] * C + vg % C) * H;
+  }
+  __syncwarp();  // ph, tt
+  double2 ar[3], ai[3];
+  // stage A (as the M2L's): Re/Im M'_n^m = SA_re/im[m][k] Re/Im (e^{-ik phi} M_n^k)
+  {
+    Frag cur;
+    double2 bc[FRAG_KS_MAX];
+    auto load_b = [&](double2* b, int n) {
+      const int ks = frag_ks(n), hb = n * (n + 1) / 2;
+#pragma unroll
+      for (int t = 0; t < FRAG_KS_MAX; ++t)
+        if (t < ks) {
+          const int col = t * 4 + fc;
+          b[t] = (msrc && col <= n) ? __ldg(msrc + hb + col) : make_double2(0.0, 0.0);
+        }
+    };
+    load(cur, 0);
+    load_b(bc, 0);
+#pragma unroll
+    for (int n = 0; n <= P; ++n) {
+      Frag nxt;
+      double2 bn[FRAG_KS_MAX];
+      if (n < P) {
+        load(nxt, n + 1);
+        load_b(bn, n + 1);
+      }
+      const int mt = frag_mt(n), ks = frag_ks(n);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) ar[q] = ai[q] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < FRAG_KS_MAX; ++t)
+        if (t < ks) {
+          const int col = t * 4 + fc;
+          const double2 x = col <= n ? cmul(ph[col], bc[t]) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (q < mt) {
+              dmma(ar[q], cur.r[q][t], x.x);
+              dmma(ai[q], cur.i[q][t], x.y);
+            }
+        }
+      const int hb = n * (n + 1) / 2;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int m = q * 8 + fr;
+        if (q < mt && m <= n) {
+          *reinterpret_cast<double2*>(bre + (hb + m) * 8 + 2 * fc) = ar[q];
+          *reinterpret_cast<double2*>(bim + (hb + m) * 8 + 2 * fc) = ai[q];
+        }
+      }
+      if (n < P) {
+        cur = nxt;
+#pragma unroll
+        for (int t = 0; t < FRAG_KS_MAX; ++t) bc[t] = bn[t];
+      }
+    }
+  }
+  Frag cur;
+  load(cur, 0);  // stage C's first degree lands during stage B
+  __syncwarp();
+  // stage B: per order k, rows n = k..P (output degree), reduction over j = k..n
+#pragma unroll
+  for (int k0 = 0; k0 <= P; k0 += 2) {
+    double2 br_[2][3], bi_[2][3];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int k = k0 + w;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) br_[w][q] = bi_[w][q] = make_double2(0.0, 0.0);
+      if (k > P) continue;
+      const int L = P + 1 - k, jt = (L + 7) >> 3, ks = (L + 3) >> 2;
+#pragma unroll
+      for (int t = 0; t < FRAG_KS_MAX; ++t)
+        if (t < ks) {
+          const int j = k + t * 4 + fc;  // input degree
+          const bool ok = j <= P;
+          const int hn = j * (j + 1) / 2 + k;
+          const double vr = ok ? bre[hn * 8 + fr] : 0.0;
+          const double vi = ok ? bim[hn * 8 + fr] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (q < jt) {
+              const int n = k + q * 8 + fr;  // output degree
+              const double a = (ok && n <= P && j <= n) ? tt[n - j] : 0.0;
+              dmma(br_[w][q], a, vr);
+              dmma(bi_[w][q], a, vi);
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int k = k0 + w;
+      if (k > P) continue;
+      const int jt = (P + 1 - k + 7) >> 3;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int n = k + q * 8 + fr;
+        if (q < jt && n <= P) {
+          const int hj = n * (n + 1) / 2 + k;
+          *reinterpret_cast<double2*>(bre + hj * 8 + 2 * fc) = br_[w][q];
+          *reinterpret_cast<double2*>(bim + hj * 8 + 2 * fc) = bi_[w][q];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // stage C: back rotation with the stage-A tables, (-1)^k on the input, (-1)^m e^{+im phi}
+  // on the output; lane owns vectors v0 + 2 fc and v0 + 2 fc + 1
+  double2* dst[2];
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const int vg = v0 + 2 * fc + w;
+    dst[w] = vg < nvec ? cout + ((size_t)child[it.y + vg / C] * C + vg % C) * H : nullptr;
+  }
+#pragma unroll
+  for (int n = 0; n <= P; ++n) {
+    Frag nxt;
+    if (n < P) load(nxt, n + 1);
+    const int mt = frag_mt(n), ks = frag_ks(n), hb = n * (n + 1) / 2;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) ar[q] = ai[q] = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int t = 0; t < FRAG_KS_MAX; ++t)
+      if (t < ks) {
+        const int col = t * 4 + fc;
+        const double sg = (col & 1) ? -1.0 : 1.0;
+        const double br = col <= n ? sg * bre[(hb + col) * 8 + fr] : 0.0;
+        const double bi = col <= n ? sg * bim[(hb + col) * 8 + fr] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (q < mt) {
+            dmma(ar[q], cur.r[q][t], br);
+            dmma(ai[q], cur.i[q][t], bi);
+          }
+      }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int m = q * 8 + fr;
+      if (q < mt && m <= n) {
+        const double2 e = cconj(ph[m]);
+        const double sg = (m & 1) ? -1.0 : 1.0;
+        if (dst[0]) dst[0][hb + m] = cscale(cmul(e, make_double2(ar[q].x, ai[q].x)), sg);
+        if (dst[1]) dst[1][hb + m] = cscale(cmul(e, make_double2(ar[q].y, ai[q].y)), sg);
+      }
+    }
+    if (n < P) cur = nxt;
+  }
+}
+
+template <int P>
+void launch_m2m_rot_p(const Plan& plan, const int4* items, int n_items, int C, const double2* M,
+                      double2* cout, cudaStream_t st) {
+  constexpr int H = hcount(P);
+  const size_t smem = (size_t)ROT_WARPS * (16 * H + 4 * P + 4) * sizeof(double);
+  static DeviceOnce attr;
+  if (attr.first()) {
+    FMM_CUDA(cudaFuncSetAttribute(k_m2m_rot<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr.mark();
+  }
+  const int64_t units = (int64_t)n_items * C;
+  k_m2m_rot<P><<<(unsigned)((units + ROT_WARPS - 1) / ROT_WARPS), ROT_WARPS * 32, smem, st>>>(
+      items, n_items, plan.m2m_rchild.get(), plan.m2m_rotf.get(), plan.m2m_dir.get(),
+      frag_base(plan.m2m_rot_p + 1), plan.m2m_aux.get(), plan.m2m_rot_p, M, C, cout);
+  FMM_LAUNCH_CHECK();
+}
+
+template <int... Ps>
+void launch_m2m_rot_dispatch(std::integer_sequence<int, Ps...>, int p, const Plan& plan,
+                             const int4* items, int n_items, int C, const double2* M, double2* cout,
+                             cudaStream_t st) {
+  bool done = false;
+  ((p == Ps + M2L_ROT_MIN_P && !done
+        ? (launch_m2m_rot_p<Ps + M2L_ROT_MIN_P>(plan, items, n_items, C, M, cout, st), done = true)
+        : false),
+   ...);
+  FMM_REQUIRE(done, "rotation M2M order out of range");
+}
 }  // namespace
 
 void compute_rot_tables(const double* d_off, int n_off, int P, double* out, double* geo,
@@ -489,6 +751,69 @@ void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int 
   FMM_REQUIRE(p <= plan.rot_p, "rotation tables not prepared for this order");
   launch_rot_dispatch(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, plan, gitems,
                       gpair, n_items, C, M, pout, st, cls);
+}
+
+void plan_ensure_m2m_rot(Plan& plan, int p, cudaStream_t s) {
+  FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
+  if (plan.m2m_rot_p >= p) return;
+  const Tree& S = plan.src;
+  // rtab id i = level * 8 + octant: d = c_child - c_parent = (+-h, +-h, +-h), h = level_half
+  const int nl = std::max(S.n_levels, 1), n_off = nl * 8;
+  std::vector<double> off(3 * (size_t)n_off);
+  for (int l = 0; l < nl; ++l)
+    for (int o = 0; o < 8; ++o) {
+      const double h = l < (int)S.level_half.size() ? S.level_half[l] : 1.0;
+      double* d = &off[3 * (size_t)(l * 8 + o)];
+      d[0] = (o & 1) ? h : -h;
+      d[1] = (o & 2) ? h : -h;
+      d[2] = (o & 4) ? h : -h;
+    }
+  std::map<double, int> dirs;
+  std::vector<int> dir(n_off);
+  std::vector<double> rep;
+  for (int u = 0; u < n_off; ++u) {
+    const double x = off[3 * u], y = off[3 * u + 1], z = off[3 * u + 2];
+    const double key = z / std::sqrt(x * x + y * y + z * z);
+    auto it = dirs.find(key);
+    if (it == dirs.end()) {
+      it = dirs.emplace(key, (int)dirs.size()).first;
+      rep.insert(rep.end(), {x, y, z});
+    }
+    dir[u] = it->second;
+  }
+  const int nd = (int)dirs.size();
+  DevBuf<double> d_rep, d_off, geo_rep, geo, one, rot;
+  d_rep.upload(rep, s);
+  d_off.upload(off, s);
+  plan.m2m_dir.upload(dir, s);
+  rot.resize((size_t)nd * rot_size(p));
+  geo_rep.resize((size_t)nd * 3);
+  compute_rot_tables(d_rep.get(), nd, p, rot.get(), geo_rep.get(), s);
+  geo.resize((size_t)n_off * 3);
+  one.resize((size_t)n_off);
+  compute_rot_tables(d_off.get(), n_off, 0, one.get(), geo.get(), s);
+  plan.m2m_rotf.resize((size_t)nd * rot_frag_size(p));
+  build_rot_frag(rot.get(), nd, p, plan.m2m_rotf.get(), s);
+  plan.m2m_aux.resize((size_t)n_off * rot_aux_size(p));
+  const int64_t n = (int64_t)n_off * aux_stride(p);
+  k_m2m_aux<<<grid_for(n, 128), 128, 0, s>>>(geo.get(), n_off, p, plan.m2m_aux.get());
+  FMM_LAUNCH_CHECK();
+  FMM_CUDA(cudaStreamSynchronize(s));
+  plan.m2m_rot_p = p;
+}
+
+void launch_m2m_rot(const Plan& plan, int p, int C, double2* M, double2* cout, cudaStream_t st) {
+  FMM_REQUIRE(p >= M2L_ROT_MIN_P && p <= plan.m2m_rot_p, "rotation M2M tables not prepared");
+  const int CH = C * hcount(p);
+  for (int l = (int)plan.m2m_level_off.size() - 2; l >= 0; --l) {
+    const int np = plan.m2m_level_off[l + 1] - plan.m2m_level_off[l];
+    if (np <= 0) continue;
+    const int ia = plan.m2m_ritem_off[l], ib = plan.m2m_ritem_off[l + 1];
+    if (ib > ia)
+      launch_m2m_rot_dispatch(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, plan,
+                              plan.d_m2m_ritems.get() + ia, ib - ia, C, M, cout, st);
+    launch_children_sum(plan, l, CH, cout, M, st);
+  }
 }
 
 }  // namespace fmmbem

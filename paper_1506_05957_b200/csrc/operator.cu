@@ -381,6 +381,24 @@ void clear_graphs(BemOp& op) {
   op.graph_kernels.clear();
 }
 
+// M2M levels above the leaves: rotation (DMMA, O(p^3)) from p = 3, octant-grouped dense below
+// (FMMBEM_M2M=grouped forces the dense kernel)
+bool m2m_rot_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FMMBEM_M2M");
+    return !(e && std::string(e) == "grouped");
+  }();
+  return on;
+}
+
+void launch_upward_m2m(BemOp& op, int p, int C, cudaStream_t s) {
+  Plan& pl = op.plan;
+  if (m2m_rot_enabled() && p >= M2L_ROT_MIN_P && pl.m2m_rot_p >= p)
+    launch_m2m_rot(pl, p, C, op.M.get(), op.m2m_cout.get(), s);
+  else
+    launch_m2m_grouped(pl, p, C, pl.rshift_src.get(), op.M.get(), op.m2m_cout.get(), s);
+}
+
 // allocations and p-dependent tables; never called inside a stream capture.
 void prepare(BemOp& op, int kind, int p, bool dense) {
   FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p must be in [0, 20]");
@@ -401,6 +419,7 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
     op.m2l_part.ensure((size_t)std::max(op.plan.n_m2l, 1) * C * hcount(p));
     plan_ensure_igrid(op.plan, p, op.s_main);
     if (op.plan.use_rot) plan_ensure_rot(op.plan, p, op.s_main);
+    if (m2m_rot_enabled()) plan_ensure_m2m_rot(op.plan, p, op.s_main);
     if (kind == op.basis_kind_for_sys) op.use_basis = ensure_p2m_basis(op, p, op.s_main);
   }
 }
@@ -628,14 +647,14 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
       // and the M2M chain above them
       launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, nullptr, 0);
       if (op.basis_leaf_only)
-        launch_m2m_grouped(pl, c.p, C, pl.rshift_src.get(), op.M.get(), op.m2m_cout.get(), s);
+        launch_upward_m2m(op, c.p, C, s);
     } else {
       if (basis)
         launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, lv, nlv);
       else
         launch_p2m(S, lv, nlv, c.p, C, q, d, op.M.get(), s);
       if (own_only) shard_exchange_multipoles(op, C, c.p, s);
-      launch_m2m_grouped(pl, c.p, C, pl.rshift_src.get(), op.M.get(), op.m2m_cout.get(), s);
+      launch_upward_m2m(op, c.p, C, s);
     }
     record(op, ST_UP, true, s);
     record(op, ST_M2L, false, s);
@@ -706,7 +725,9 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
                                           (const void*)(intptr_t)op.plan.igrid_p,
                                           (const void*)(intptr_t)op.basis_p,
                                           (const void*)(intptr_t)op.plan.n_rot_dirs,
-                                          (const void*)(intptr_t)op.basis_cols};
+                                          (const void*)(intptr_t)op.basis_cols,
+                                          op.plan.m2m_rotf.get(), op.plan.m2m_aux.get(),
+                                          (const void*)(intptr_t)op.plan.m2m_rot_p};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;

@@ -618,7 +618,9 @@ void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const dou
   int dev = 0, sms = 0;
   FMM_CUDA(cudaGetDevice(&dev));
   FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = std::min(aux.n_items, sms);
+  // FMMBEM_P2P_RESERVE=k leaves k SMs without a near-field CTA (for the far-field chain)
+  static const int reserve = std::getenv("FMMBEM_P2P_RESERVE") ? std::atoi(std::getenv("FMMBEM_P2P_RESERVE")) : 0;
+  const int grid = std::min(aux.n_items, std::max(1, sms - reserve));
   if (grid > 0)
     kern<<<grid, nthr, smem, st>>>(T, aux.hdr.get(), aux.n_items, aux.ltab.get(), aux.slot.get(),
                                    aux.spec.get(), max_src,

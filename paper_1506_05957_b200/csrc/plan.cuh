@@ -134,6 +134,16 @@ struct Plan {
   DevBuf<int4> d_m2m_gitems;
   DevBuf<int> m2m_gchild;
 
+  // rotation-based M2M (m2l_rot.cu): children grouped by (level, octant) in items of <= 8,
+  // per parent level [m2m_ritem_off[l], m2m_ritem_off[l+1]); per rtab id (level * 8 + octant)
+  // the rotation fragments of its direction and (e^{-ik phi}, |d|^l / l!)
+  std::vector<int> m2m_ritem_off;
+  DevBuf<int4> d_m2m_ritems;
+  DevBuf<int> m2m_rchild;
+  DevBuf<double> m2m_rotf, m2m_aux;
+  DevBuf<int> m2m_dir;
+  int m2m_rot_p = -1;
+
   // M2M / L2L translation tables: R(d) for the 8 child octants of every level, up to igrid... P_MAX
   DevBuf<double2> rshift_src;  // [level][octant][(P_MAX+1)^2] full storage
   DevBuf<double2> rshift_tgt;
@@ -145,6 +155,7 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
 // (re)build the irregular-harmonic tables for M2L up to order 2p
 void plan_ensure_igrid(Plan& plan, int p, cudaStream_t s);
 void plan_ensure_rot(Plan& plan, int p, cudaStream_t s);
+void plan_ensure_m2m_rot(Plan& plan, int p, cudaStream_t s);
 // item indices by decreasing work (targets x sources), for the persistent P2P kernel
 std::vector<int> p2p_schedule(const Tree& T, const Tree& S, const std::vector<P2PItem>& items,
                               const std::vector<int>& p2p_src);

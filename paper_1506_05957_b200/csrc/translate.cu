@@ -814,6 +814,15 @@ void launch_m2m_grouped(const Plan& plan, int p, int C, const double2* rfull, do
   }
 }
 
+void launch_children_sum(const Plan& plan, int l, int CH, const double2* cout, double2* M,
+                         cudaStream_t st) {
+  const int np = plan.m2m_level_off[l + 1] - plan.m2m_level_off[l];
+  if (np <= 0) return;
+  k_children_sum<<<np, 128, 0, st>>>(plan.m2m_cells.get() + plan.m2m_level_off[l],
+                                     plan.src.first_child.get(), plan.src.n_child.get(), CH, cout, M);
+  FMM_LAUNCH_CHECK();
+}
+
 void launch_m2m(const Tree& S, const std::vector<int>& level_off, const int* cells, int p, int C,
                 const double2* rfull, double2* M, cudaStream_t st) {
   TrArgs a{};

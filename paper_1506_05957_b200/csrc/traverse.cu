@@ -416,9 +416,10 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
     }
     plan.m2m_cells.upload(cells.empty() ? std::vector<int>(1, 0) : cells, s);
     // children of those parents grouped by (level, octant) -> shared R(d)
-    std::vector<int4> gitems;
-    std::vector<int> gchild;
+    std::vector<int4> gitems, ritems;
+    std::vector<int> gchild, rchild;
     plan.m2m_gitem_off.assign(1, 0);
+    plan.m2m_ritem_off.assign(1, 0);
     for (int l = 0; l < S.n_levels; ++l) {
       std::vector<std::vector<int>> by_oct(8);
       for (int k = plan.m2m_level_off[l]; k < plan.m2m_level_off[l + 1]; ++k) {
@@ -436,9 +437,17 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
           for (size_t j = i; j < std::min(v.size(), i + 4); ++j) gchild.push_back(v[j]);
           gitems.push_back(make_int4((l + 1) * 8 + o, b, (int)gchild.size(), 0));
         }
+        for (size_t i = 0; i < v.size(); i += 8) {  // rotation M2M: 8 vectors per warp
+          const int b = (int)rchild.size();
+          for (size_t j = i; j < std::min(v.size(), i + 8); ++j) rchild.push_back(v[j]);
+          ritems.push_back(make_int4((l + 1) * 8 + o, b, (int)rchild.size(), 0));
+        }
       }
       plan.m2m_gitem_off.push_back((int)gitems.size());
+      plan.m2m_ritem_off.push_back((int)ritems.size());
     }
+    plan.d_m2m_ritems.upload(ritems.empty() ? std::vector<int4>(1) : ritems, s);
+    plan.m2m_rchild.upload(rchild.empty() ? std::vector<int>(1, 0) : rchild, s);
     plan.d_m2m_gitems.upload(gitems.empty() ? std::vector<int4>(1) : gitems, s);
     plan.m2m_gchild.upload(gchild.empty() ? std::vector<int>(1, 0) : gchild, s);
     for (int c = 0; c < T.n_cells; ++c)
