@@ -50,6 +50,7 @@ constexpr int M2L_ROT_MIN_P = 3;  // rotation-based M2L from this order up
 // M2M by rotation (point and shoot, DMMA): per-child contributions into cout, then the
 // children of every parent summed in order (p >= M2L_ROT_MIN_P; plan_ensure_m2m_rot first)
 void launch_m2m_rot(const Plan& plan, int p, int C, double2* M, double2* cout, cudaStream_t st);
+void launch_l2l_rot(const Plan& plan, int p, int C, double2* L, cudaStream_t st);
 void launch_children_sum(const Plan& plan, int level, int CH, const double2* cout, double2* M,
                          cudaStream_t st);
 // M2M through octant-grouped child translations (cout: per-cell child contributions)

@@ -491,15 +491,24 @@ __global__ void k_m2m_aux(const double* __restrict__ geo, int n_off, int P, doub
 }
 
 // warp unit = (item, octet of vectors); vector v of an item = (child v / C, channel v % C);
-// the item's children share one rtab id (level, octant): one direction, phase and |d|
-template <int P>
+// the item's children share one rtab id (level, octant): one direction, phase and |d|.
+// LOCAL = false: M2M (above), the child's multipole -> its contribution to the parent's,
+//                written to the child's slot of cout (k_children_sum adds them in order).
+// LOCAL = true:  L2L, the parent's local expansion -> ADDED to the child's (harmonics.py:
+//   175-176): rotate the local with (A^{-1})^T = a~^T E^{+} (SC tables, checkerboard sign,
+//   input phase e^{+ik phi}), translate along z with the upper-triangular Toeplitz
+//   L''_n^k = sum_{j>=n} |d|^{j-n}/(j-n)! L'_j^k, and rotate back with A^T = E a^T (the M2L's
+//   stage C).
+template <int P, bool LOCAL>
 __global__ void __launch_bounds__(ROT_WARPS * 32)
-k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ child,
-          const double* __restrict__ frag, const int* __restrict__ dir, int ttot,
-          const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
-          double2* __restrict__ cout) {
+k_vrot(const int4* __restrict__ items, int n_items, const int* __restrict__ child,
+       const int* __restrict__ parent, const double* __restrict__ frag, const int* __restrict__ dir,
+       int ttot, const double* __restrict__ aux, int aux_p, const double2* __restrict__ in, int C,
+       double2* __restrict__ out) {
   constexpr int H = hcount(P);
   constexpr int WS = 16 * H + 4 * P + 4;
+  constexpr int TAB_IN = LOCAL ? 2 : 0;   // fragments of the first rotation
+  constexpr int TAB_OUT = LOCAL ? 2 : 0;  // and of the back rotation
   extern __shared__ double sh[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x * ROT_WARPS + warp;
@@ -523,9 +532,9 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
   }
   const int fr = lane >> 2, fc = lane & 3;
   const double* T = frag + (size_t)dir[u] * 4 * ttot * 32 + lane;
-  auto load = [&](Frag& f, int n) {  // stage-A tables (SA_re, SA_im) of degree n
+  auto load = [&](Frag& f, int tab, int n) {
     const int mt = frag_mt(n), ks = frag_ks(n);
-    const double* tr = T + (size_t)frag_base(n) * 32;
+    const double* tr = T + (size_t)(tab * ttot + frag_base(n)) * 32;
     const double* ti = tr + (size_t)ttot * 32;
 #pragma unroll
     for (int q = 0; q < 3; ++q)
@@ -536,14 +545,17 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
           f.i[q][t] = __ldg(ti + (q * ks + t) * 32);
         }
   };
-  const double2* msrc = nullptr;
+  const double2* vsrc = nullptr;
   {
     const int vg = v0 + fr;
-    if (vg < nvec) msrc = M + ((size_t)child[it.y + vg / C] * C + vg % C) * H;
+    if (vg < nvec) {
+      const int c = child[it.y + vg / C];
+      vsrc = in + ((size_t)(LOCAL ? parent[c] : c) * C + vg % C) * H;
+    }
   }
   __syncwarp();  // ph, tt
   double2 ar[3], ai[3];
-  // stage A (as the M2L's): Re/Im M'_n^m = SA_re/im[m][k] Re/Im (e^{-ik phi} M_n^k)
+  // stage 1: first rotation, degree by degree
   {
     Frag cur;
     double2 bc[FRAG_KS_MAX];
@@ -553,17 +565,17 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
       for (int t = 0; t < FRAG_KS_MAX; ++t)
         if (t < ks) {
           const int col = t * 4 + fc;
-          b[t] = (msrc && col <= n) ? __ldg(msrc + hb + col) : make_double2(0.0, 0.0);
+          b[t] = (vsrc && col <= n) ? __ldg(vsrc + hb + col) : make_double2(0.0, 0.0);
         }
     };
-    load(cur, 0);
+    load(cur, TAB_IN, 0);
     load_b(bc, 0);
 #pragma unroll
     for (int n = 0; n <= P; ++n) {
       Frag nxt;
       double2 bn[FRAG_KS_MAX];
       if (n < P) {
-        load(nxt, n + 1);
+        load(nxt, TAB_IN, n + 1);
         load_b(bn, n + 1);
       }
       const int mt = frag_mt(n), ks = frag_ks(n);
@@ -573,7 +585,12 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
       for (int t = 0; t < FRAG_KS_MAX; ++t)
         if (t < ks) {
           const int col = t * 4 + fc;
-          const double2 x = col <= n ? cmul(ph[col], bc[t]) : make_double2(0.0, 0.0);
+          double2 x = make_double2(0.0, 0.0);
+          if (col <= n) {
+            // M2M: e^{-ik phi} M; L2L: (-1)^k e^{+ik phi} L
+            x = LOCAL ? cmul(cconj(ph[col]), bc[t]) : cmul(ph[col], bc[t]);
+            if (LOCAL && (col & 1)) x = make_double2(-x.x, -x.y);
+          }
 #pragma unroll
           for (int q = 0; q < 3; ++q)
             if (q < mt) {
@@ -586,8 +603,13 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
       for (int q = 0; q < 3; ++q) {
         const int m = q * 8 + fr;
         if (q < mt && m <= n) {
-          *reinterpret_cast<double2*>(bre + (hb + m) * 8 + 2 * fc) = ar[q];
-          *reinterpret_cast<double2*>(bim + (hb + m) * 8 + 2 * fc) = ai[q];
+          double2 r = ar[q], i = ai[q];
+          if (LOCAL && (m & 1)) {  // output checkerboard sign of a~^T
+            r = make_double2(-r.x, -r.y);
+            i = make_double2(-i.x, -i.y);
+          }
+          *reinterpret_cast<double2*>(bre + (hb + m) * 8 + 2 * fc) = r;
+          *reinterpret_cast<double2*>(bim + (hb + m) * 8 + 2 * fc) = i;
         }
       }
       if (n < P) {
@@ -598,9 +620,10 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
     }
   }
   Frag cur;
-  load(cur, 0);  // stage C's first degree lands during stage B
+  load(cur, TAB_OUT, 0);  // the back rotation's first degree lands during stage 2
   __syncwarp();
-  // stage B: per order k, rows n = k..P (output degree), reduction over j = k..n
+  // stage 2: z translation per order k, rows n = k..P (output degree), columns j (input degree):
+  // M2M lower-triangular t_{n-j} (j <= n), L2L upper-triangular t_{j-n} (j >= n)
 #pragma unroll
   for (int k0 = 0; k0 <= P; k0 += 2) {
     double2 br_[2][3], bi_[2][3];
@@ -614,7 +637,7 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
 #pragma unroll
       for (int t = 0; t < FRAG_KS_MAX; ++t)
         if (t < ks) {
-          const int j = k + t * 4 + fc;  // input degree
+          const int j = k + t * 4 + fc;
           const bool ok = j <= P;
           const int hn = j * (j + 1) / 2 + k;
           const double vr = ok ? bre[hn * 8 + fr] : 0.0;
@@ -622,8 +645,12 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
 #pragma unroll
           for (int q = 0; q < 3; ++q)
             if (q < jt) {
-              const int n = k + q * 8 + fr;  // output degree
-              const double a = (ok && n <= P && j <= n) ? tt[n - j] : 0.0;
+              const int n = k + q * 8 + fr;
+              double a = 0.0;
+              if (ok && n <= P) {
+                if (LOCAL) a = j >= n ? tt[j - n] : 0.0;
+                else a = j <= n ? tt[n - j] : 0.0;
+              }
               dmma(br_[w][q], a, vr);
               dmma(bi_[w][q], a, vi);
             }
@@ -647,18 +674,19 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
     }
     __syncwarp();
   }
-  // stage C: back rotation with the stage-A tables, (-1)^k on the input, (-1)^m e^{+im phi}
-  // on the output; lane owns vectors v0 + 2 fc and v0 + 2 fc + 1
+  // stage 3: back rotation; lane owns vectors v0 + 2 fc and v0 + 2 fc + 1
+  // M2M: (-1)^m e^{+im phi} (SA with (-1)^k on the input), written to the child's slot;
+  // L2L: e^{-ik phi} (SC), added to the child's local expansion
   double2* dst[2];
 #pragma unroll
   for (int w = 0; w < 2; ++w) {
     const int vg = v0 + 2 * fc + w;
-    dst[w] = vg < nvec ? cout + ((size_t)child[it.y + vg / C] * C + vg % C) * H : nullptr;
+    dst[w] = vg < nvec ? out + ((size_t)child[it.y + vg / C] * C + vg % C) * H : nullptr;
   }
 #pragma unroll
   for (int n = 0; n <= P; ++n) {
     Frag nxt;
-    if (n < P) load(nxt, n + 1);
+    if (n < P) load(nxt, TAB_OUT, n + 1);
     const int mt = frag_mt(n), ks = frag_ks(n), hb = n * (n + 1) / 2;
 #pragma unroll
     for (int q = 0; q < 3; ++q) ar[q] = ai[q] = make_double2(0.0, 0.0);
@@ -666,7 +694,7 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
     for (int t = 0; t < FRAG_KS_MAX; ++t)
       if (t < ks) {
         const int col = t * 4 + fc;
-        const double sg = (col & 1) ? -1.0 : 1.0;
+        const double sg = (!LOCAL && (col & 1)) ? -1.0 : 1.0;
         const double br = col <= n ? sg * bre[(hb + col) * 8 + fr] : 0.0;
         const double bi = col <= n ? sg * bim[(hb + col) * 8 + fr] : 0.0;
 #pragma unroll
@@ -680,44 +708,59 @@ k_m2m_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ c
     for (int q = 0; q < 3; ++q) {
       const int m = q * 8 + fr;
       if (q < mt && m <= n) {
-        const double2 e = cconj(ph[m]);
-        const double sg = (m & 1) ? -1.0 : 1.0;
-        if (dst[0]) dst[0][hb + m] = cscale(cmul(e, make_double2(ar[q].x, ai[q].x)), sg);
-        if (dst[1]) dst[1][hb + m] = cscale(cmul(e, make_double2(ar[q].y, ai[q].y)), sg);
+        if (LOCAL) {
+          const double2 e = ph[m];
+          if (dst[0]) dst[0][hb + m] = cadd(dst[0][hb + m], cmul(e, make_double2(ar[q].x, ai[q].x)));
+          if (dst[1]) dst[1][hb + m] = cadd(dst[1][hb + m], cmul(e, make_double2(ar[q].y, ai[q].y)));
+        } else {
+          const double2 e = cconj(ph[m]);
+          const double sg = (m & 1) ? -1.0 : 1.0;
+          if (dst[0]) dst[0][hb + m] = cscale(cmul(e, make_double2(ar[q].x, ai[q].x)), sg);
+          if (dst[1]) dst[1][hb + m] = cscale(cmul(e, make_double2(ar[q].y, ai[q].y)), sg);
+        }
       }
     }
     if (n < P) cur = nxt;
   }
 }
 
-template <int P>
-void launch_m2m_rot_p(const Plan& plan, const int4* items, int n_items, int C, const double2* M,
-                      double2* cout, cudaStream_t st) {
+struct VrotTabs {  // one tree's rotation tables (Plan::m2m_* or Plan::l2l_*)
+  const int4* items;
+  const int* child;
+  const int* parent;
+  const double* frag;
+  const int* dir;
+  const double* aux;
+  int p;
+};
+
+template <int P, bool LOCAL>
+void launch_vrot_p(const VrotTabs& t, int ia, int n_items, int C, const double2* in, double2* out,
+                   cudaStream_t st) {
   constexpr int H = hcount(P);
   const size_t smem = (size_t)ROT_WARPS * (16 * H + 4 * P + 4) * sizeof(double);
   static DeviceOnce attr;
   if (attr.first()) {
-    FMM_CUDA(cudaFuncSetAttribute(k_m2m_rot<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    FMM_CUDA(cudaFuncSetAttribute(k_vrot<P, LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr.mark();
   }
   const int64_t units = (int64_t)n_items * C;
-  k_m2m_rot<P><<<(unsigned)((units + ROT_WARPS - 1) / ROT_WARPS), ROT_WARPS * 32, smem, st>>>(
-      items, n_items, plan.m2m_rchild.get(), plan.m2m_rotf.get(), plan.m2m_dir.get(),
-      frag_base(plan.m2m_rot_p + 1), plan.m2m_aux.get(), plan.m2m_rot_p, M, C, cout);
+  k_vrot<P, LOCAL><<<(unsigned)((units + ROT_WARPS - 1) / ROT_WARPS), ROT_WARPS * 32, smem, st>>>(
+      t.items + ia, n_items, t.child, t.parent, t.frag, t.dir, frag_base(t.p + 1), t.aux, t.p, in, C, out);
   FMM_LAUNCH_CHECK();
 }
 
-template <int... Ps>
-void launch_m2m_rot_dispatch(std::integer_sequence<int, Ps...>, int p, const Plan& plan,
-                             const int4* items, int n_items, int C, const double2* M, double2* cout,
-                             cudaStream_t st) {
+template <bool LOCAL, int... Ps>
+void launch_vrot_dispatch(std::integer_sequence<int, Ps...>, int p, const VrotTabs& t, int ia,
+                          int n_items, int C, const double2* in, double2* out, cudaStream_t st) {
   bool done = false;
   ((p == Ps + M2L_ROT_MIN_P && !done
-        ? (launch_m2m_rot_p<Ps + M2L_ROT_MIN_P>(plan, items, n_items, C, M, cout, st), done = true)
+        ? (launch_vrot_p<Ps + M2L_ROT_MIN_P, LOCAL>(t, ia, n_items, C, in, out, st), done = true)
         : false),
    ...);
-  FMM_REQUIRE(done, "rotation M2M order out of range");
+  FMM_REQUIRE(done, "rotation M2M/L2L order out of range");
 }
+
 }  // namespace
 
 void compute_rot_tables(const double* d_off, int n_off, int P, double* out, double* geo,
@@ -753,16 +796,17 @@ void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int 
                       gpair, n_items, C, M, pout, st, cls);
 }
 
-void plan_ensure_m2m_rot(Plan& plan, int p, cudaStream_t s) {
-  FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
-  if (plan.m2m_rot_p >= p) return;
-  const Tree& S = plan.src;
-  // rtab id i = level * 8 + octant: d = c_child - c_parent = (+-h, +-h, +-h), h = level_half
-  const int nl = std::max(S.n_levels, 1), n_off = nl * 8;
+namespace {
+
+// per rtab id (level * 8 + octant) of one tree: d = c_child - c_parent = (+-h, +-h, +-h),
+// h = the child level's half width; fragments per distinct polar angle, (phase, |d|^l/l!) rows
+void build_vrot_tables(const Tree& tr, int p, DevBuf<double>& frag_out, DevBuf<int>& dir_out,
+                       DevBuf<double>& aux_out, cudaStream_t s) {
+  const int nl = std::max(tr.n_levels, 1), n_off = nl * 8;
   std::vector<double> off(3 * (size_t)n_off);
   for (int l = 0; l < nl; ++l)
     for (int o = 0; o < 8; ++o) {
-      const double h = l < (int)S.level_half.size() ? S.level_half[l] : 1.0;
+      const double h = l < (int)tr.level_half.size() ? tr.level_half[l] : 1.0;
       double* d = &off[3 * (size_t)(l * 8 + o)];
       d[0] = (o & 1) ? h : -h;
       d[1] = (o & 2) ? h : -h;
@@ -785,35 +829,57 @@ void plan_ensure_m2m_rot(Plan& plan, int p, cudaStream_t s) {
   DevBuf<double> d_rep, d_off, geo_rep, geo, one, rot;
   d_rep.upload(rep, s);
   d_off.upload(off, s);
-  plan.m2m_dir.upload(dir, s);
+  dir_out.upload(dir, s);
   rot.resize((size_t)nd * rot_size(p));
   geo_rep.resize((size_t)nd * 3);
   compute_rot_tables(d_rep.get(), nd, p, rot.get(), geo_rep.get(), s);
   geo.resize((size_t)n_off * 3);
   one.resize((size_t)n_off);
   compute_rot_tables(d_off.get(), n_off, 0, one.get(), geo.get(), s);
-  plan.m2m_rotf.resize((size_t)nd * rot_frag_size(p));
-  build_rot_frag(rot.get(), nd, p, plan.m2m_rotf.get(), s);
-  plan.m2m_aux.resize((size_t)n_off * rot_aux_size(p));
+  frag_out.resize((size_t)nd * rot_frag_size(p));
+  build_rot_frag(rot.get(), nd, p, frag_out.get(), s);
+  aux_out.resize((size_t)n_off * rot_aux_size(p));
   const int64_t n = (int64_t)n_off * aux_stride(p);
-  k_m2m_aux<<<grid_for(n, 128), 128, 0, s>>>(geo.get(), n_off, p, plan.m2m_aux.get());
+  k_m2m_aux<<<grid_for(n, 128), 128, 0, s>>>(geo.get(), n_off, p, aux_out.get());
   FMM_LAUNCH_CHECK();
   FMM_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+void plan_ensure_m2m_rot(Plan& plan, int p, cudaStream_t s) {
+  FMM_REQUIRE(p >= 0 && p <= P_MAX, "expansion order p out of range [0, 20]");
+  if (plan.m2m_rot_p >= p) return;
+  build_vrot_tables(plan.src, p, plan.m2m_rotf, plan.m2m_dir, plan.m2m_aux, s);
+  build_vrot_tables(plan.tgt, p, plan.l2l_rotf, plan.l2l_dir, plan.l2l_aux, s);
   plan.m2m_rot_p = p;
 }
 
 void launch_m2m_rot(const Plan& plan, int p, int C, double2* M, double2* cout, cudaStream_t st) {
   FMM_REQUIRE(p >= M2L_ROT_MIN_P && p <= plan.m2m_rot_p, "rotation M2M tables not prepared");
   const int CH = C * hcount(p);
+  const VrotTabs t{plan.d_m2m_ritems.get(), plan.m2m_rchild.get(), plan.src.parent.get(),
+                   plan.m2m_rotf.get(), plan.m2m_dir.get(), plan.m2m_aux.get(), plan.m2m_rot_p};
   for (int l = (int)plan.m2m_level_off.size() - 2; l >= 0; --l) {
     const int np = plan.m2m_level_off[l + 1] - plan.m2m_level_off[l];
     if (np <= 0) continue;
     const int ia = plan.m2m_ritem_off[l], ib = plan.m2m_ritem_off[l + 1];
     if (ib > ia)
-      launch_m2m_rot_dispatch(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, plan,
-                              plan.d_m2m_ritems.get() + ia, ib - ia, C, M, cout, st);
+      launch_vrot_dispatch<false>(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, t,
+                                  ia, ib - ia, C, M, cout, st);
     launch_children_sum(plan, l, CH, cout, M, st);
   }
 }
 
+void launch_l2l_rot(const Plan& plan, int p, int C, double2* L, cudaStream_t st) {
+  FMM_REQUIRE(p >= M2L_ROT_MIN_P && p <= plan.m2m_rot_p, "rotation L2L tables not prepared");
+  const VrotTabs t{plan.d_l2l_ritems.get(), plan.l2l_rchild.get(), plan.tgt.parent.get(),
+                   plan.l2l_rotf.get(), plan.l2l_dir.get(), plan.l2l_aux.get(), plan.m2m_rot_p};
+  for (int l = 0; l + 1 < (int)plan.l2l_ritem_off.size(); ++l) {  // top-down
+    const int ia = plan.l2l_ritem_off[l], ib = plan.l2l_ritem_off[l + 1];
+    if (ib > ia)
+      launch_vrot_dispatch<true>(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, t,
+                                 ia, ib - ia, C, L, L, st);
+  }
+}
 }  // namespace fmmbem

@@ -391,6 +391,24 @@ bool m2m_rot_enabled() {
   return on;
 }
 
+// downward pass: rotation L2L down the target tree, then each leaf's own expansion at its
+// targets (the reference's L2L + L2P, fmm.py:280-336), or (FMMBEM_DOWN=path, the sharded
+// path, p < 3) every path cell's expansion evaluated at the leaf's targets (L2L is exact)
+// The L2L levels are a chain of short, latency-bound launches (~15-20 us each at p = 14); they
+// pay off only when the path epilogue's per-target work is large: cfg5 (4 088 target leaves,
+// ~80 targets each): 0.29 -> 0.11 + 0.10 ms per p = 14 apply; cfg2 / cfg3 (272 leaves): slower.
+constexpr int L2L_MIN_TGT_LEAVES = 1024;
+
+bool l2l_rot_mode(const BemOp& op, int p, bool sharded, bool dense) {
+  static const int force = [] {  // FMMBEM_DOWN=l2l | path
+    const char* e = std::getenv("FMMBEM_DOWN");
+    return !e ? -1 : std::string(e) == "path" ? 0 : 1;
+  }();
+  const bool want = force >= 0 ? force == 1 : op.plan.tgt.n_leaves >= L2L_MIN_TGT_LEAVES;
+  return want && !sharded && !dense && m2m_rot_enabled() && p >= M2L_ROT_MIN_P &&
+         op.plan.m2m_rot_p >= p;
+}
+
 void launch_upward_m2m(BemOp& op, int p, int C, cudaStream_t s) {
   Plan& pl = op.plan;
   if (m2m_rot_enabled() && p >= M2L_ROT_MIN_P && pl.m2m_rot_p >= p)
@@ -556,9 +574,10 @@ void launch_layer_epilogue(BemOp& op, const LayerCall& c, bool sharded, cudaStre
   const int n_epi = sharded ? sw.n_epi_leaves : pl.tgt.n_leaves;
   a.part = c.dense ? op.part_dense.get() : op.part.get();
   a.L = op.L.get();
-  a.path_off = pl.epi_path_off.get();
-  a.path = pl.epi_path.get();
-  a.max_path = pl.max_path;
+  const bool l2l = l2l_rot_mode(op, c.p, sharded, c.dense);
+  a.path_off = l2l ? pl.epi_leaf_off.get() : pl.epi_path_off.get();
+  a.path = l2l ? pl.epi_leaf.get() : pl.epi_path.get();
+  a.max_path = l2l ? 1 : pl.max_path;
   a.p = c.p;
   a.rowptr = op.near_rowptr.get();
   a.rows = op.near_rows.get();
@@ -665,7 +684,8 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     else
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);
-    record(op, ST_DOWN, false, s);  // (no L2L levels: the epilogue walks each leaf's path)
+    record(op, ST_DOWN, false, s);
+    if (l2l_rot_mode(op, c.p, sharded, c.dense)) launch_l2l_rot(pl, c.p, C, op.L.get(), s);
     record(op, ST_DOWN, true, s);
   }
   if (!serial) FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
@@ -727,6 +747,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
                                           (const void*)(intptr_t)op.plan.n_rot_dirs,
                                           (const void*)(intptr_t)op.basis_cols,
                                           op.plan.m2m_rotf.get(), op.plan.m2m_aux.get(),
+                                          op.plan.l2l_rotf.get(), op.plan.l2l_aux.get(),
                                           (const void*)(intptr_t)op.plan.m2m_rot_p};
     if (sig != op.graph_sig) {
       clear_graphs(op);

@@ -142,7 +142,16 @@ struct Plan {
   DevBuf<int> m2m_rchild;
   DevBuf<double> m2m_rotf, m2m_aux;
   DevBuf<int> m2m_dir;
-  int m2m_rot_p = -1;
+  int m2m_rot_p = -1;  // (both trees' tables: M2M on the source tree, L2L on the target tree)
+  // rotation-based L2L on the target tree: the cells of l2l_cells grouped by (level, octant),
+  // items of <= 8, per level (top-down); with it the epilogue evaluates only each leaf's own
+  // (complete) local expansion: epi_leaf_off / epi_leaf (the leaf, or nothing without far field)
+  std::vector<int> l2l_ritem_off;
+  DevBuf<int4> d_l2l_ritems;
+  DevBuf<int> l2l_rchild;
+  DevBuf<double> l2l_rotf, l2l_aux;
+  DevBuf<int> l2l_dir;
+  DevBuf<int> epi_leaf_off, epi_leaf;
 
   // M2M / L2L translation tables: R(d) for the 8 child octants of every level, up to igrid... P_MAX
   DevBuf<double2> rshift_src;  // [level][octant][(P_MAX+1)^2] full storage

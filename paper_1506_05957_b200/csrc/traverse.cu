@@ -463,6 +463,37 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
       plan.l2l_level_off.push_back((int)cells.size());
     }
     plan.l2l_cells.upload(cells.empty() ? std::vector<int>(1, 0) : cells, s);
+    {
+      std::vector<int4> ritems;
+      std::vector<int> rchild;
+      plan.l2l_ritem_off.assign(1, 0);
+      for (int l = 0; l < T.n_levels; ++l) {
+        std::vector<std::vector<int>> by_oct(8);
+        for (int k = plan.l2l_level_off[l]; k < plan.l2l_level_off[l + 1]; ++k) {
+          const int c = cells[k], par = T.h_parent[c];
+          const int o = (T.h_cx[c] > T.h_cx[par] ? 1 : 0) | (T.h_cy[c] > T.h_cy[par] ? 2 : 0) |
+                        (T.h_cz[c] > T.h_cz[par] ? 4 : 0);
+          by_oct[o].push_back(c);
+        }
+        for (int o = 0; o < 8; ++o)
+          for (size_t i = 0; i < by_oct[o].size(); i += 8) {
+            const int b = (int)rchild.size();
+            for (size_t j = i; j < std::min(by_oct[o].size(), i + 8); ++j) rchild.push_back(by_oct[o][j]);
+            ritems.push_back(make_int4(l * 8 + o, b, (int)rchild.size(), 0));
+          }
+        plan.l2l_ritem_off.push_back((int)ritems.size());
+      }
+      plan.d_l2l_ritems.upload(ritems.empty() ? std::vector<int4>(1) : ritems, s);
+      plan.l2l_rchild.upload(rchild.empty() ? std::vector<int>(1, 0) : rchild, s);
+      std::vector<int> loff(T.n_cells + 1, 0), leaf;
+      for (int c = 0; c < T.n_cells; ++c) {
+        loff[c] = (int)leaf.size();
+        if (T.h_n_child[c] == 0 && nz[c]) leaf.push_back(c);
+      }
+      loff[T.n_cells] = (int)leaf.size();
+      plan.epi_leaf_off.upload(loff, s);
+      plan.epi_leaf.upload(leaf.empty() ? std::vector<int>(1, 0) : leaf, s);
+    }
     std::vector<int> poff(T.n_cells + 1, 0), path;
     for (int c = 0; c < T.n_cells; ++c) {
       poff[c] = (int)path.size();
