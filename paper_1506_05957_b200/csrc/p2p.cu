@@ -196,7 +196,7 @@ k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __rest
 // ~eps R^2 / r^2 <= ~1e-12 relative on the closest pairs.  The coincident pair (the target is
 // Gauss point 0 of its own panel, bemop.py:64-67; the reference's d2 > 0 mask, fmm.py:403) is
 // removed by index: its slot in the staged tile gets d2 = ~1e300, so r^-3 underflows to 0.
-// 13 DP instructions per interaction (15 in the difference form).
+// 12 DP instructions per interaction (15 in the difference form).
 //
 // Persistent and warp-specialised: one CTA per SM; LAPD_PROD producer warps take items in
 // largest-first order from a global counter and stage item k+1 (leaf table, transformed
@@ -280,11 +280,13 @@ __device__ __forceinline__ void lapd_body(const LapdSrc& u, int j, const double*
     if (MASK) d2 = __hiloint2double(j == self[q] ? 0x7E37E43C : __double2hiint(d2), __double2loint(d2));
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
+    // r^-3 = y^3 (1 + 3/2 e), e = 1 - d2 y^2, = -3/2 y^3 g with g = d2 y^2 - 5/3; the -3/2
+    // is folded into the staged dipoles (rn below is -3/2 d.(t - y)): 12 DP instructions
     const double y2 = y * y;
+    const double g = fma(d2, y2, -5.0 / 3.0);
     const double y3 = y2 * y;
-    const double e = fma(-d2, y2, 1.0);
     const double rn = fma(u.dxy.x, tx[q], fma(u.dxy.y, ty[q], fma(u.dzs.x, tz[q], u.dzs.y)));
-    acc[q] = fma(rn, fma(1.5 * e, y3, y3), acc[q]);
+    acc[q] = fma(rn * y3, g, acc[q]);
   }
 }
 
@@ -378,8 +380,10 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
         }
         const int dst = (r < H.nspec && spec[r] == i) ? r : H.nspec + i - r;
         const double sx = v[u][0].x - H.cx, sy = v[u][0].y - H.cy, sz = v[u][1].x - H.cz;
-        // dipole d = (w n) x[panel] (bemop.py:188-203, 213-216)
-        const double dx = v[u][1].y * xv[u], dy = v[u][2].x * xv[u], dz = v[u][2].y * xv[u];
+        // dipole d = (w n) x[panel] (bemop.py:188-203, 213-216), times the -3/2 of the
+        // interaction body's r^-3 = -3/2 y^3 g
+        const double xs = -1.5 * xv[u];
+        const double dx = v[u][1].y * xs, dy = v[u][2].x * xs, dz = v[u][2].y * xs;
         const double ss = fma(sx, sx, fma(sy, sy, sz * sz));
         const double ds = fma(dx, sx, fma(dy, sy, dz * sz));
         sh2[dst] = make_double2(-2.0 * sx, -2.0 * sy);

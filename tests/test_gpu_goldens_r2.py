@@ -21,11 +21,13 @@ pytestmark = pytest.mark.gpu
 _OPS = {}
 
 
-def _op(name, upward=None):
+def _op(name, upward=None, **env):
+    """Operator of a config; upward / env select kernel variants (read at construction and at
+    the first apply: FMMBEM_UPWARD direct|leaf, FMMBEM_DOWN path|l2l, FMMBEM_M2M grouped)."""
     from paper_1506_05957_b200.configs import CONFIGS
     from paper_1506_05957_b200.operator import GpuBemOperator
 
-    key = (name, upward)
+    key = (name, upward, tuple(sorted(env.items())))
     if key not in _OPS:
         cfg = CONFIGS[name]
         old = os.environ.pop("FMMBEM_UPWARD", None)
@@ -110,3 +112,29 @@ def test_cfg4_relaxed_gmres_matches_reference():
     np.testing.assert_allclose(res.residuals[:k], g["relaxed_residuals"][:k], rtol=1e-5)
     assert rel_l2(res.x[g["rows"]], g["relaxed_x_rows"]) <= 1e-6
     assert abs(np.linalg.norm(res.x) / float(g["relaxed_x_norm"]) - 1.0) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_downward_modes_agree(name):
+    """Rotation L2L + leaf-only epilogue vs the path epilogue (L2L is exact): run in a
+    subprocess each, since the mode switch is read once per process."""
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "from paper_1506_05957_b200.configs import CONFIGS;"
+            "from paper_1506_05957_b200.operator import GpuBemOperator;"
+            f"cfg = CONFIGS['{name}'];"
+            "op = GpuBemOperator(cfg.mesh(), cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu);"
+            "x = np.random.default_rng(1).uniform(-1, 1, op.shape[0]);"
+            "np.save(sys.argv[1], np.stack([op.apply(x, p) for p in (3, 5, 12)]))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("path", "l2l"):
+        f = os.path.join(root, "gpurun_out", f"down_{name}_{mode}.npy")
+        os.makedirs(os.path.dirname(f), exist_ok=True)
+        subprocess.run([sys.executable, "-c", code, f], cwd=root, check=True,
+                       env=dict(os.environ, FMMBEM_DOWN=mode))
+        out[mode] = np.load(f)
+    for k in range(3):
+        assert rel_l2(out["l2l"][k], out["path"][k]) <= 1e-12, k
