@@ -278,6 +278,8 @@ __device__ __forceinline__ void lapd_body(const LapdSrc& u, int j, const double*
     double d2 = fma(tx[q], u.ab.x, fma(ty[q], u.ab.y, fma(tz[q], u.cs.x, u.cs.y + tt[q])));
     // coincident pair: hi word of ~1e300 (the lo word is irrelevant), so r^-3 underflows to 0
     if (MASK) d2 = __hiloint2double(j == self[q] ? 0x7E37E43C : __double2hiint(d2), __double2loint(d2));
+    // seed: MUFU.RSQ64H (an fp32 MUFU.RSQ seed through F2F conversions measured 16 % slower
+    // on cfg5: the conversions cost more FP64-pipe time than the fp64 seed)
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
     // r^-3 = y^3 (1 + 3/2 e), e = 1 - d2 y^2, = -3/2 y^3 g with g = d2 y^2 - 5/3; the -3/2
@@ -606,7 +608,7 @@ long long* p2p_trace_buffer() {
 void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const double2* srec,
                      const int* s_panel, const double* x, double* part, cudaStream_t st, unsigned* sched) {
   const LapdStage L(max_src, aux.max_leaves, aux.max_tgt);
-  static const int nct = std::getenv("FMMBEM_P2P_NCT") ? std::atoi(std::getenv("FMMBEM_P2P_NCT")) : LAPD_CONS;
+  constexpr int nct = LAPD_CONS;
   const size_t per = L.bytes + (size_t)nct * LAPD_TPT * sizeof(double);
   // 2 stages: measured faster than 3 inside the concurrent step (the far-field kernels share the
   // SMs' shared memory with this persistent kernel); FMMBEM_P2P_STAGES=3 for a deeper ring
@@ -615,9 +617,8 @@ void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const dou
   const size_t smem = nstg * per;
   FMM_REQUIRE(smem <= 227 * 1024, "P2P: source slice too large for shared memory");
   FMM_REQUIRE(sched != nullptr, "P2P: the double-layer kernel needs its schedule counter");
-  auto kern = nstg == 3 ? (nct == 384 ? k_p2p_lapd<384, 3> : k_p2p_lapd<LAPD_CONS, 3>)
-                        : (nct == 384 ? k_p2p_lapd<384, 2> : k_p2p_lapd<LAPD_CONS, 2>);
-  const int nthr = (nct == 384 ? nct : LAPD_CONS) + LAPD_PROD;
+  auto kern = nstg == 3 ? k_p2p_lapd<LAPD_CONS, 3> : k_p2p_lapd<LAPD_CONS, 2>;
+  const int nthr = LAPD_CONS + LAPD_PROD;
   FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 0;
   FMM_CUDA(cudaGetDevice(&dev));
