@@ -166,8 +166,10 @@ int fmmbem_op_counters(fmmbem_op* op, int64_t* kernel_launches, int64_t* applies
  * rank r owns target leaves [tleaf_bounds[r], tleaf_bounds[r+1]) and source
  * leaves [sleaf_bounds[r], sleaf_bounds[r+1]) (leaf indices in body order, bounds of length
  * world+1).  Each apply does P2M of its source leaves, an NCCL all-gather of the leaf
- * multipoles, M2L/L2L/P2P/epilogue for its target leaves and an NCCL all-gather of the
- * result; GMRES then runs replicated.  nccl_id: 128 bytes from fmmbem_nccl_unique_id on rank
+ * multipoles, M2L/L2L/P2P/epilogue for its target leaves and (fmmbem_op_apply) an NCCL
+ * all-gather of the result.  fmmbem_op_gmres on a sharded op partitions the Krylov vectors:
+ * each rank keeps its own rows, all-gathers v_k before each apply and reduces the
+ * Gram-Schmidt dot products with NCCL all-reduces (CGS2); x is returned whole on every rank.  nccl_id: 128 bytes from fmmbem_nccl_unique_id on rank
  * 0, shared by the caller (e.g. torch.distributed); NULL = "virtual" shard without
  * collectives that computes only its own rows (single-GPU check of the work split). */
 int fmmbem_nccl_unique_id(unsigned char* out128);
@@ -177,6 +179,17 @@ int fmmbem_op_leaf_work(const fmmbem_op* op, int which, double* w);
 int fmmbem_op_shard(fmmbem_op* op, int rank, int world, const int32_t* tleaf_bounds,
                     const int32_t* sleaf_bounds, const unsigned char* nccl_id);
 int fmmbem_op_unshard(fmmbem_op* op);
+/* The same partition with a caller-provided HOST transport instead of NCCL: every collective
+ * of the sharded apply and GMRES copies its device buffer to pinned host memory, calls the
+ * callback, and copies the result back.  allgather: recv (world * count) = every rank's send
+ * (count) in rank order; allreduce: buf (count) summed over ranks in place.  Return 0 on
+ * success.  Used for two processes sharing one GPU (tests, with torch.distributed/gloo behind
+ * the callbacks) and for transports without NCCL; the apply then runs without CUDA graphs. */
+typedef int (*fmmbem_allgather_fn)(const double* send, double* recv, int64_t count, void* user);
+typedef int (*fmmbem_allreduce_fn)(double* buf, int64_t count, void* user);
+int fmmbem_op_shard_host(fmmbem_op* op, int rank, int world, const int32_t* tleaf_bounds,
+                         const int32_t* sleaf_bounds, fmmbem_allgather_fn allgather,
+                         fmmbem_allreduce_fn allreduce, void* user);
 
 #ifdef __cplusplus
 }

@@ -80,11 +80,20 @@ SIGNATURES = {
     "fmmbem_op_shard": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _c_int32_p, _c_int32_p,
                                        ctypes.c_char_p]),
     "fmmbem_op_unshard": (ctypes.c_int, [_vp]),
+    "fmmbem_op_shard_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _c_int32_p, _c_int32_p,
+                                            _vp, _vp, _vp]),
 }
 
 # int (*)(int32_t k, double residual, int32_t p, void* user)  (fmmbem_gmres_callback)
 GMRES_CALLBACK = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
                                   ctypes.c_void_p)
+
+# int (*)(const double* send, double* recv, int64_t count, void* user)  (fmmbem_allgather_fn)
+ALLGATHER_CALLBACK = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                      ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p)
+# int (*)(double* buf, int64_t count, void* user)  (fmmbem_allreduce_fn)
+ALLREDUCE_CALLBACK = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                                      ctypes.c_void_p)
 
 _lib = None
 

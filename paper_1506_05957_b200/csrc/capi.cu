@@ -523,6 +523,16 @@ int fmmbem_op_shard(fmmbem_op* h, int rank, int world, const int32_t* tleaf_boun
   });
 }
 
+int fmmbem_op_shard_host(fmmbem_op* h, int rank, int world, const int32_t* tleaf_bounds,
+                         const int32_t* sleaf_bounds, fmmbem_allgather_fn allgather,
+                         fmmbem_allreduce_fn allreduce, void* user) {
+  return guarded([&] {
+    FMM_REQUIRE(h && tleaf_bounds && sleaf_bounds && allgather && allreduce, "null argument");
+    select(h->device);
+    op_shard_setup_host(*h->op, rank, world, tleaf_bounds, sleaf_bounds, allgather, allreduce, user);
+  });
+}
+
 int fmmbem_op_unshard(fmmbem_op* h) {
   return guarded([&] {
     FMM_REQUIRE(h, "null argument");

@@ -353,6 +353,185 @@ int schedule_p(double r, double eta, int p_initial, int p_min) {
   return std::min(p_initial, std::max(p_min, p));
 }
 
+
+// ---- partitioned GMRES (a real shard, one process per GPU) ----------------
+// Each rank keeps only its own rows of the Krylov vectors (sorted target order, as the sharded
+// epilogue writes them).  Per iteration: all-gather of v_k into the apply's input, the apply
+// (own rows of w), classical Gram-Schmidt with one re-orthogonalisation (CGS2: two batched
+// all-reduces of k+1 local dot products, then one of ||w||^2), and the same Givens update on
+// every rank (bitwise-equal H after the all-reduces).  CGS2 replaces the reference's MGS
+// (solver.py:100-103) by an algebraically equal, roundoff-level different sweep.
+constexpr int SB = 256, SG = 2 * 148;  // threads / blocks of the partitioned vector kernels
+
+__device__ double block_sum_sb(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < SB / 32; ++i) t += sh[i];
+  __syncthreads();
+  return t;
+}
+
+// part[j * SG + block] = partial dot of V_j and w (grid (SG, k1))
+__global__ void __launch_bounds__(SB) k_sh_dots(int64_t n, const double* __restrict__ V,
+                                                const double* __restrict__ w, double* __restrict__ part) {
+  __shared__ double sh[SB / 32];
+  const int j = blockIdx.y;
+  const double* v = V + (size_t)j * n;
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)SB + threadIdx.x; i < n; i += (int64_t)SG * SB)
+    acc = fma(v[i], w[i], acc);
+  acc = block_sum_sb(acc, sh);
+  if (threadIdx.x == 0) part[(size_t)j * SG + blockIdx.x] = acc;
+}
+
+// h[j] = sum of the partials in block order (fixed: identical on every call)
+__global__ void k_sh_finish(int k1, const double* __restrict__ part, double* __restrict__ h) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k1) return;
+  double t = 0.0;
+  for (int b = 0; b < SG; ++b) t += part[(size_t)j * SG + b];
+  h[j] = t;
+}
+
+// w -= sum_j h_j V_j
+__global__ void k_sh_update(int64_t n, int k1, const double* __restrict__ V, const double* __restrict__ h,
+                            double* __restrict__ w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = w[i];
+    for (int j = 0; j < k1; ++j) acc = fma(-h[j], V[(size_t)j * n + i], acc);
+    w[i] = acc;
+  }
+}
+
+__global__ void k_sh_scale(int64_t n, const double* __restrict__ w, double inv, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = w[i] * inv;
+}
+
+GmresResult op_gmres_sharded(BemOp& op, const double* b, double tol, double eta, int p_initial,
+                             int p_min, bool relaxed, int max_iter, double* x, GmresCallback cb,
+                             void* user) {
+  ShardWork& sw = op.shard;
+  GmresResult res;
+  cudaStream_t s = op.s_main;
+  const int nc = op.formulation == STOKES ? 3 : 1;
+  const int64_t nl = (int64_t)(sw.tbody_b - sw.tbody_a) * nc;  // own rows
+  const int64_t nv = std::max<int64_t>(nl, 1);
+  DevBuf<double>& V = op.g_basis;
+  V.ensure((size_t)(max_iter + 2) * nv);
+  DevBuf<double>& part = op.g_partials;
+  part.ensure((size_t)SG * (max_iter + 1));
+  DevBuf<double>& scal = op.g_scal;
+  scal.ensure(2 * (size_t)(max_iter + 2));
+  double* h1 = scal.get();
+  double* h2 = scal.get() + (max_iter + 2);
+  double* w = V.get() + (size_t)(max_iter + 1) * nv;  // scratch column
+  auto dots = [&](const double* Vb, int k1, const double* vec, double* h) {
+    if (nl > 0) k_sh_dots<<<dim3(SG, k1), SB, 0, s>>>(nl, Vb, vec, part.get());
+    else FMM_CUDA(cudaMemsetAsync(part.get(), 0, (size_t)SG * k1 * sizeof(double), s));
+    k_sh_finish<<<grid_for(k1, 128), 128, 0, s>>>(k1, part.get(), h);
+    FMM_LAUNCH_CHECK();
+    shard_allreduce(op, h, k1, s);
+  };
+  auto read = [&](const double* d, int k1, double* hst) {
+    FMM_CUDA(cudaMemcpyAsync(hst, d, k1 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+  };
+  // own rows of b, ||b||
+  shard_pack_rows(op, nc, b, w, s);
+  double nb2 = 0.0;
+  dots(w, 1, w, h1);
+  read(h1, 1, &nb2);
+  const double norm_b = std::sqrt(nb2);
+  if (norm_b == 0.0 || max_iter == 0) {
+    FMM_CUDA(cudaMemsetAsync(x, 0, op.n * sizeof(double), s));
+    FMM_CUDA(cudaStreamSynchronize(s));
+    res.converged = norm_b == 0.0;
+    return res;
+  }
+  k_sh_scale<<<RB, RT, 0, s>>>(nl, w, 1.0 / norm_b, V.get());
+  FMM_LAUNCH_CHECK();
+  std::vector<double> H((size_t)(max_iter + 1) * max_iter, 0.0);
+  auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * max_iter + j]; };
+  std::vector<double> cs(max_iter), sn(max_iter), g(max_iter + 1, 0.0), ha(max_iter + 1), hb(max_iter + 1);
+  g[0] = norm_b;
+  double residual = 1.0;
+  int prev_p = p_initial;
+  sw.local_vectors = true;
+  try {
+    for (int k = 0; k < max_iter; ++k) {
+      const int p = relaxed ? std::min(schedule_p(residual, eta, p_initial, p_min), prev_p) : p_initial;
+      prev_p = p;
+      const double* vk = V.get() + (size_t)k * nv;
+      double* vk1 = V.get() + (size_t)(k + 1) * nv;
+      // all-gather v_k into the apply's (panel-order) input; the apply leaves w's own rows in ysend
+      shard_gather_rows(op, nc, vk, op.x_in.get(), s);
+      op_apply_device(op, nullptr, nullptr, p);
+      if (nl > 0)
+        FMM_CUDA(cudaMemcpyAsync(w, sw.ysend.get(), nl * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      // CGS2
+      dots(V.get(), k + 1, w, h1);
+      k_sh_update<<<RB, RT, 0, s>>>(nl, k + 1, V.get(), h1, w);
+      dots(V.get(), k + 1, w, h2);
+      k_sh_update<<<RB, RT, 0, s>>>(nl, k + 1, V.get(), h2, w);
+      double ww = 0.0;
+      dots(w, 1, w, h2 + k + 1);
+      read(h1, k + 1, ha.data());
+      read(h2, k + 2, hb.data());
+      ww = hb[k + 1];
+      const double hk1 = std::sqrt(ww);
+      k_sh_scale<<<RB, RT, 0, s>>>(nl, w, hk1 > 0.0 ? 1.0 / hk1 : 0.0, vk1);
+      FMM_LAUNCH_CHECK();
+      op.kernel_launches += 8;
+      for (int j = 0; j <= k; ++j) Hat(j, k) = ha[j] + hb[j];
+      Hat(k + 1, k) = hk1;
+      for (int j = 0; j < k; ++j) {
+        const double t1 = cs[j] * Hat(j, k) + sn[j] * Hat(j + 1, k);
+        Hat(j + 1, k) = -sn[j] * Hat(j, k) + cs[j] * Hat(j + 1, k);
+        Hat(j, k) = t1;
+      }
+      const double denom = std::hypot(Hat(k, k), Hat(k + 1, k));
+      cs[k] = Hat(k, k) / denom;
+      sn[k] = Hat(k + 1, k) / denom;
+      Hat(k, k) = denom;
+      Hat(k + 1, k) = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      residual = std::fabs(g[k + 1]) / norm_b;
+      res.residuals.push_back(residual);
+      res.orders.push_back(p);
+      if (cb && cb(k + 1, residual, p, user) != 0) {
+        res.stopped = true;
+        break;
+      }
+      if (residual < tol) {
+        res.converged = true;
+        break;
+      }
+    }
+  } catch (...) {
+    sw.local_vectors = false;
+    throw;
+  }
+  sw.local_vectors = false;
+  const int m = (int)res.orders.size();
+  std::vector<double> y(std::max(m, 1), 0.0);
+  for (int i = m - 1; i >= 0; --i) {
+    double t = g[i];
+    for (int j = i + 1; j < m; ++j) t -= Hat(i, j) * y[j];
+    y[i] = t / Hat(i, i);
+  }
+  DevBuf<double>& yd = op.g_y;
+  yd.upload(y, s);
+  k_combine<<<RB, RT, 0, s>>>(nl, m, V.get(), yd.get(), w);
+  FMM_LAUNCH_CHECK();
+  shard_gather_rows(op, nc, w, x, s);  // every rank returns the whole solution
+  op.kernel_launches += 2;
+  return res;
+}
 }  // namespace
 
 GmresResult op_gmres(BemOp& op, const double* b, double tol, double eta, int p_initial, int p_min,
@@ -363,6 +542,9 @@ GmresResult op_gmres(BemOp& op, const double* b, double tol, double eta, int p_i
   FMM_REQUIRE(p_initial >= 0 && p_initial <= P_MAX, "p_initial must be in [0, 20]");
   FMM_REQUIRE(!(op.shard.active && op.shard.virtual_mode),
               "GMRES needs full mat-vecs: a virtual shard only computes its own rows");
+  FMM_REQUIRE(max_iter >= 0, "max_iter must be >= 0");
+  if (op.shard.active)
+    return op_gmres_sharded(op, b, tol, eta, p_initial, p_min, relaxed, max_iter, x, cb, user);
   GmresResult res;
   const int64_t n = op.n;
   cudaStream_t s = op.s_main;

@@ -438,6 +438,11 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
     plan_ensure_igrid(op.plan, p, op.s_main);
     if (op.plan.use_rot) plan_ensure_rot(op.plan, p, op.s_main);
     if (m2m_rot_enabled()) plan_ensure_m2m_rot(op.plan, p, op.s_main);
+    if (op.shard.active && !op.shard.virtual_mode) {  // exchange buffers (no allocation in a capture)
+      const size_t per = (size_t)op.shard.max_sleaves * C * hcount(p);
+      op.shard.mleaf_send.ensure(std::max<size_t>(per, 1));
+      op.shard.mleaf_recv.ensure(std::max<size_t>(per * op.shard.world, 1));
+    }
     if (kind == op.basis_kind_for_sys) op.use_basis = ensure_p2m_basis(op, p, op.s_main);
   }
 }
@@ -691,7 +696,8 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   if (!serial) FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
   launch_layer_epilogue(op, c, sharded, s, split_epi ? 2 : 0);
   const bool ysorted_out = sharded && !sw.virtual_mode;
-  if (ysorted_out) shard_exchange_y(op, c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE ? 1 : 3, c.y, s);
+  if (ysorted_out && !sw.local_vectors)
+    shard_exchange_y(op, c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE ? 1 : 3, c.y, s);
   record(op, ST_EPI, true, s);
   record(op, ST_TOTAL, true, s);
 }
@@ -731,7 +737,9 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
   cudaStream_t s = op.s_main;
   if (x) FMM_CUDA(cudaMemcpyAsync(op.x_in.get(), x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   const bool sharded = op.shard.active;
-  if (op.use_graphs && !(sharded && !op.shard.virtual_mode)) {
+  // graphs: unsharded, virtual and NCCL shards (NCCL collectives are captured); the host
+  // transport blocks the host inside every collective and runs eagerly
+  if (op.use_graphs && !(sharded && op.shard.transport == ShardWork::T_HOST)) {
     // captured graphs bake in buffer addresses: any reallocation invalidates them
     const std::vector<const void*> sig = {op.q.get(), op.dip.get(), op.wsrc.get(), op.srec.get(), op.part.get(),
                                           op.M.get(), op.L.get(), op.plan.igrid.get(),
@@ -748,12 +756,14 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
                                           (const void*)(intptr_t)op.basis_cols,
                                           op.plan.m2m_rotf.get(), op.plan.m2m_aux.get(),
                                           op.plan.l2l_rotf.get(), op.plan.l2l_aux.get(),
-                                          (const void*)(intptr_t)op.plan.m2m_rot_p};
+                                          (const void*)(intptr_t)op.plan.m2m_rot_p,
+                                          op.shard.mleaf_send.get(), op.shard.mleaf_recv.get(),
+                                          op.shard.ysend.get(), op.shard.yrecv.get()};
     if (sig != op.graph_sig) {
       clear_graphs(op);
       op.graph_sig = sig;
     }
-    const int key = p * 4 + (op.timing ? 1 : 0) + (op.serial_near ? 2 : 0);
+    const int key = p * 8 + (op.timing ? 1 : 0) + (op.serial_near ? 2 : 0) + (op.shard.local_vectors ? 4 : 0);
     auto it = op.graphs.find(key);
     if (it == op.graphs.end()) {
       cudaGraph_t g;
@@ -786,6 +796,7 @@ void op_apply_device(BemOp& op, const double* x, double* y, int p) {
     op.applies += 1;
   } else {
     op_layer(op, c, s, sharded);
+    op.applies += 1;
   }
   if (y) FMM_CUDA(cudaMemcpyAsync(y, op.y_out.get(), op.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }

@@ -23,9 +23,25 @@ enum Stage : int { ST_P2P = 0, ST_UP = 1, ST_M2L = 2, ST_DOWN = 3, ST_EPI = 4, S
 
 // One rank's share of a partitioned apply (shard.cu): target leaves
 // [tleaf_a, tleaf_b) and source leaves [sleaf_a, sleaf_b) in body order.
+// host-staged collectives (fmmbem_op_shard_host): the caller's transport on host buffers
+typedef int (*HostAllgather)(const double* send, double* recv, int64_t count, void* user);
+typedef int (*HostAllreduce)(double* buf, int64_t count, void* user);
+
 struct ShardWork {
   bool active = false;
   bool virtual_mode = false;  // no collectives: full upward pass, own y entries only (tests)
+  // transport of a real shard: NCCL (device buffers, capturable in the per-p graphs) or the
+  // caller's host callbacks (device <-> pinned host staging around each collective)
+  enum Transport : int { T_VIRTUAL = 0, T_NCCL = 1, T_HOST = 2 };
+  int transport = T_VIRTUAL;
+  HostAllgather host_ag = nullptr;
+  HostAllreduce host_ar = nullptr;
+  void* host_user = nullptr;
+  double* hstage = nullptr;  // pinned host staging of the host transport
+  size_t hstage_cap = 0;
+  // partitioned Krylov vectors (sharded GMRES): the apply consumes the gathered x_in and
+  // leaves its own rows in ysend (sorted target order) instead of all-gathering y
+  bool local_vectors = false;
   int rank = 0, world = 1;
   int tleaf_a = 0, tleaf_b = 0, tbody_a = 0, tbody_b = 0, max_tbody = 0;
   int sleaf_a = 0, sleaf_b = 0, max_sleaves = 0;
@@ -195,6 +211,7 @@ void op_dense_apply_device(BemOp& op, const double* x, double* y);
 void op_rhs_device(BemOp& op, const double* data, double* b, int p, bool dense);
 void build_near_pairs(BemOp& op, cudaStream_t s);
 bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s);  // false: over the memory budget
+void prepare_p2m_leaf_items(BemOp& op, const int* leaves_dev, int n_leaves);
 void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cudaStream_t s,
                       const int* leaves = nullptr, int n_leaves = -1);
 void build_correction(BemOp& op, int kind, Correction& out, cudaStream_t s);
@@ -212,6 +229,15 @@ void op_shard_release(BemOp& op);
 void op_leaf_work(const BemOp& op, int which, double* w);
 void shard_exchange_multipoles(BemOp& op, int C, int p, cudaStream_t s);
 void shard_exchange_y(BemOp& op, int nc, double* y, cudaStream_t s);
+// collectives of a real shard (NCCL or the host transport), stream-ordered on s
+void shard_allgather(BemOp& op, const double* send, double* recv, size_t count, cudaStream_t s);
+void shard_allreduce(BemOp& op, double* buf, size_t count, cudaStream_t s);
+// own rows (sorted target order, nc per target) of a panel-order vector, and the inverse
+// all-gather of every rank's rows into a panel-order vector
+void shard_pack_rows(const BemOp& op, int nc, const double* full, double* local, cudaStream_t s);
+void shard_gather_rows(BemOp& op, int nc, const double* local, double* full, cudaStream_t s);
+void op_shard_setup_host(BemOp& op, int rank, int world, const int* tleaf_bounds,
+                         const int* sleaf_bounds, HostAllgather ag, HostAllreduce ar, void* user);
 void nccl_unique_id(unsigned char* out);
 
 // per-iteration progress (solver.py:122-123): k (1-based), residual, p; nonzero return stops

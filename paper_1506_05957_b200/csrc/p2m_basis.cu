@@ -367,6 +367,18 @@ bool ensure_p2m_basis(BemOp& op, int p, cudaStream_t s) {
   return true;
 }
 
+// the work items of a shard's own leaves for the clustered basis (host data: call outside a
+// stream capture, e.g. when the shard is set up)
+void prepare_p2m_leaf_items(BemOp& op, const int* leaves, int n_leaves) {
+  if (!op.basis_clustered || leaves == op.p2m_leaf_list) return;
+  std::vector<int> lv(n_leaves);
+  if (n_leaves)
+    FMM_CUDA(cudaMemcpy(lv.data(), leaves, n_leaves * sizeof(int), cudaMemcpyDeviceToHost));
+  set_p2m_items(op, lv, op.h_cl_range, op.p2m_leaf_items, op.p2m_leaf_reduce, op.n_p2m_leaf_slots);
+  op.p2m_part.ensure((size_t)std::max(op.n_p2m_leaf_slots, 1) * hcount(P_MAX));
+  op.p2m_leaf_list = leaves;
+}
+
 void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cudaStream_t s,
                       const int* leaves, int n_leaves) {
   const Tree& S = op.plan.src;
@@ -374,14 +386,7 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
   if (op.basis_clustered) {
     FMM_REQUIRE(C == 1, "clustered P2M basis is single-channel");
     const bool direct = leaves == nullptr;  // all multipoles, else the given leaves
-    if (!direct && leaves != op.p2m_leaf_list) {  // a shard's leaf list (not under capture)
-      std::vector<int> lv(n_leaves);
-      if (n_leaves)
-        FMM_CUDA(cudaMemcpy(lv.data(), leaves, n_leaves * sizeof(int), cudaMemcpyDeviceToHost));
-      set_p2m_items(op, lv, op.h_cl_range, op.p2m_leaf_items, op.p2m_leaf_reduce, op.n_p2m_leaf_slots);
-      op.p2m_part.ensure((size_t)std::max(op.n_p2m_leaf_slots, 1) * hcount(P_MAX));
-      op.p2m_leaf_list = leaves;
-    }
+    if (!direct && leaves != op.p2m_leaf_list) prepare_p2m_leaf_items(op, leaves, n_leaves);
     const P2MItems& it = direct ? op.p2m_items : op.p2m_leaf_items;
     const P2MItems& red = direct ? op.p2m_reduce : op.p2m_leaf_reduce;
     FMM_REQUIRE(op.p2m_part.size() >= (size_t)std::max(op.n_p2m_slots, op.n_p2m_leaf_slots) * H,

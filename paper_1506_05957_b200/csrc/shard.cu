@@ -30,15 +30,18 @@ typedef struct { char internal[128]; } NcclId;
 typedef int (*fn_getid)(NcclId*);
 typedef int (*fn_init)(void**, int, NcclId, int);
 typedef int (*fn_allgather)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef int (*fn_allreduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*fn_destroy)(void*);
 typedef const char* (*fn_errstr)(int);
 constexpr int NCCL_DOUBLE = 8;  // ncclFloat64
+constexpr int NCCL_SUM = 0;     // ncclSum
 
 struct Nccl {
   void* h = nullptr;
   fn_getid get_id = nullptr;
   fn_init init = nullptr;
   fn_allgather allgather = nullptr;
+  fn_allreduce allreduce = nullptr;
   fn_destroy destroy = nullptr;
   fn_errstr errstr = nullptr;
   void load() {
@@ -48,9 +51,11 @@ struct Nccl {
     get_id = (fn_getid)dlsym(h, "ncclGetUniqueId");
     init = (fn_init)dlsym(h, "ncclCommInitRank");
     allgather = (fn_allgather)dlsym(h, "ncclAllGather");
+    allreduce = (fn_allreduce)dlsym(h, "ncclAllReduce");
     destroy = (fn_destroy)dlsym(h, "ncclCommDestroy");
     errstr = (fn_errstr)dlsym(h, "ncclGetErrorString");
-    if (!get_id || !init || !allgather || !destroy) throw CudaFailure("libnccl.so.2 lacks symbols");
+    if (!get_id || !init || !allgather || !allreduce || !destroy)
+      throw CudaFailure("libnccl.so.2 lacks symbols");
   }
   void check(int rc, const char* what) {
     if (rc) throw CudaFailure(std::string(what) + ": " + (errstr ? errstr(rc) : "nccl error"));
@@ -77,6 +82,15 @@ __global__ void k_unpack_leaves(const int* __restrict__ leaves, int n_leaves,
   const double2* src = recv + ((size_t)r * max_per + (li - bounds[r])) * CH;
   double2* dst = M + (size_t)leaves[li] * CH;
   for (int t = threadIdx.x; t < CH; t += blockDim.x) dst[t] = src[t];
+}
+
+// own rows of a panel-order vector in sorted target order: local[i nc + c] = full[perm[a + i] nc + c]
+__global__ void k_pack_rows(int64_t n_loc, const int* __restrict__ perm, int tbody_a, int nc,
+                            const double* __restrict__ full, double* __restrict__ local) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_loc) return;
+  const int pn = perm[tbody_a + i];
+  for (int c = 0; c < nc; ++c) local[i * nc + c] = full[(size_t)pn * nc + c];
 }
 
 // y[panel] from the gathered per-rank slices (sorted target order)
@@ -106,7 +120,77 @@ void op_shard_release(BemOp& op) {
     g_nccl.destroy(op.shard.comm);
     op.shard.comm = nullptr;
   }
+  if (op.shard.hstage) {
+    cudaFreeHost(op.shard.hstage);
+    op.shard.hstage = nullptr;
+    op.shard.hstage_cap = 0;
+  }
   op.shard.active = false;
+  op.shard.transport = ShardWork::T_VIRTUAL;
+  op.shard.local_vectors = false;
+}
+
+namespace {
+double* host_stage(ShardWork& sw, size_t n) {
+  if (sw.hstage_cap < n) {
+    if (sw.hstage) FMM_CUDA(cudaFreeHost(sw.hstage));
+    sw.hstage_cap = std::max(n, (size_t)1 << 16);
+    FMM_CUDA(cudaHostAlloc(&sw.hstage, sw.hstage_cap * sizeof(double), cudaHostAllocDefault));
+  }
+  return sw.hstage;
+}
+}  // namespace
+
+void shard_allgather(BemOp& op, const double* send, double* recv, size_t count, cudaStream_t s) {
+  ShardWork& sw = op.shard;
+  if (sw.transport == ShardWork::T_NCCL) {
+    g_nccl.check(g_nccl.allgather(send, recv, count, NCCL_DOUBLE, sw.comm, s), "ncclAllGather");
+    return;
+  }
+  FMM_REQUIRE(sw.transport == ShardWork::T_HOST && sw.host_ag, "shard has no transport");
+  double* h = host_stage(sw, count * (sw.world + 1));
+  FMM_CUDA(cudaMemcpyAsync(h, send, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  if (sw.host_ag(h, h + count, (int64_t)count, sw.host_user) != 0)
+    throw CudaFailure("host transport: all-gather failed");
+  FMM_CUDA(cudaMemcpyAsync(recv, h + count, count * sw.world * sizeof(double), cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaStreamSynchronize(s));  // the staging buffer is reused by the next collective
+}
+
+void shard_allreduce(BemOp& op, double* buf, size_t count, cudaStream_t s) {
+  ShardWork& sw = op.shard;
+  if (sw.transport == ShardWork::T_NCCL) {
+    g_nccl.check(g_nccl.allreduce(buf, buf, count, NCCL_DOUBLE, NCCL_SUM, sw.comm, s), "ncclAllReduce");
+    return;
+  }
+  FMM_REQUIRE(sw.transport == ShardWork::T_HOST && sw.host_ar, "shard has no transport");
+  double* h = host_stage(sw, count);
+  FMM_CUDA(cudaMemcpyAsync(h, buf, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  if (sw.host_ar(h, (int64_t)count, sw.host_user) != 0) throw CudaFailure("host transport: all-reduce failed");
+  FMM_CUDA(cudaMemcpyAsync(buf, h, count * sizeof(double), cudaMemcpyHostToDevice, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+}
+
+void shard_pack_rows(const BemOp& op, int nc, const double* full, double* local, cudaStream_t s) {
+  const ShardWork& sw = op.shard;
+  const int64_t nl = sw.tbody_b - sw.tbody_a;
+  if (nl > 0)
+    k_pack_rows<<<grid_for(nl, 256), 256, 0, s>>>(nl, op.plan.tgt.perm.get(), sw.tbody_a, nc, full, local);
+  FMM_LAUNCH_CHECK();
+}
+
+void shard_gather_rows(BemOp& op, int nc, const double* local, double* full, cudaStream_t s) {
+  ShardWork& sw = op.shard;
+  const size_t per = (size_t)sw.max_tbody * nc;
+  const int64_t nl = (int64_t)(sw.tbody_b - sw.tbody_a) * nc;
+  if (nl > 0 && local != sw.ysend.get())
+    FMM_CUDA(cudaMemcpyAsync(sw.ysend.get(), local, nl * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  shard_allgather(op, sw.ysend.get(), sw.yrecv.get(), per, s);
+  const Tree& T = op.plan.tgt;
+  k_unpack_y<<<grid_for(T.n_points, 256), 256, 0, s>>>(T.n_points, T.perm.get(), sw.body_owner_off.get(),
+                                                       sw.world, sw.max_tbody, nc, sw.yrecv.get(), full);
+  FMM_LAUNCH_CHECK();
 }
 
 // per-leaf work weights used by the host-side partitioner
@@ -267,6 +351,7 @@ void op_shard_setup(BemOp& op, int rank, int world, const int* tb, const int* sb
   sw.ysend.ensure((size_t)std::max(sw.max_tbody, 1) * 3);
   sw.yrecv.ensure((size_t)std::max(sw.max_tbody, 1) * 3 * world);
   // ---- communicator
+  sw.transport = sw.virtual_mode ? ShardWork::T_VIRTUAL : ShardWork::T_NCCL;
   if (!sw.virtual_mode) {
     g_nccl.load();
     NcclId id;
@@ -275,12 +360,27 @@ void op_shard_setup(BemOp& op, int rank, int world, const int* tb, const int* sb
     g_nccl.check(g_nccl.init(&sw.comm, world, id, rank), "ncclCommInitRank");
   }
   FMM_CUDA(cudaStreamSynchronize(s));
+  op.p2m_leaf_list = nullptr;  // (sw.p2m_leaves was reallocated)
+  prepare_p2m_leaf_items(op, sw.p2m_leaves.get(), sw.n_p2m_leaves);
   // graphs were captured for the unpartitioned apply
   for (auto& kv : op.graphs) cudaGraphExecDestroy(kv.second);
   op.graphs.clear();
   op.graph_kernels.clear();
   op.graph_sig.clear();
   sw.active = true;
+}
+
+void op_shard_setup_host(BemOp& op, int rank, int world, const int* tb, const int* sb,
+                         HostAllgather ag, HostAllreduce ar, void* user) {
+  FMM_REQUIRE(ag && ar, "host transport needs all-gather and all-reduce callbacks");
+  // the work split as for NCCL, built in virtual mode (no communicator), then switched over
+  op_shard_setup(op, rank, world, tb, sb, nullptr);
+  ShardWork& sw = op.shard;
+  sw.virtual_mode = false;
+  sw.transport = ShardWork::T_HOST;
+  sw.host_ag = ag;
+  sw.host_ar = ar;
+  sw.host_user = user;
 }
 
 void shard_exchange_multipoles(BemOp& op, int C, int p, cudaStream_t s) {
@@ -293,8 +393,8 @@ void shard_exchange_multipoles(BemOp& op, int C, int p, cudaStream_t s) {
     k_pack_leaves<<<sw.n_p2m_leaves, 128, 0, s>>>(sw.p2m_leaves.get(), sw.n_p2m_leaves, CH, op.M.get(),
                                                   sw.mleaf_send.get());
   FMM_LAUNCH_CHECK();
-  g_nccl.check(g_nccl.allgather(sw.mleaf_send.get(), sw.mleaf_recv.get(), per * 2, NCCL_DOUBLE,
-                                sw.comm, s), "ncclAllGather(multipoles)");
+  shard_allgather(op, reinterpret_cast<const double*>(sw.mleaf_send.get()),
+                  reinterpret_cast<double*>(sw.mleaf_recv.get()), per * 2, s);
   const Tree& S = op.plan.src;
   k_unpack_leaves<<<S.n_leaves, 128, 0, s>>>(S.leaves.get(), S.n_leaves, sw.leaf_owner_off.get(),
                                              sw.world, sw.max_sleaves, CH, sw.mleaf_recv.get(),
@@ -305,8 +405,7 @@ void shard_exchange_multipoles(BemOp& op, int C, int p, cudaStream_t s) {
 void shard_exchange_y(BemOp& op, int nc, double* y, cudaStream_t s) {
   ShardWork& sw = op.shard;
   const size_t per = (size_t)sw.max_tbody * nc;
-  g_nccl.check(g_nccl.allgather(sw.ysend.get(), sw.yrecv.get(), per, NCCL_DOUBLE, sw.comm, s),
-               "ncclAllGather(y)");
+  shard_allgather(op, sw.ysend.get(), sw.yrecv.get(), per, s);
   const Tree& T = op.plan.tgt;
   k_unpack_y<<<grid_for(T.n_points, 256), 256, 0, s>>>(T.n_points, T.perm.get(), sw.body_owner_off.get(),
                                                        sw.world, sw.max_tbody, nc, sw.yrecv.get(), y);

@@ -365,8 +365,41 @@ class GpuBemOperator:
         N.check(self._lib.fmmbem_op_shard(self._h, int(rank), int(world), N.i32ptr(tb), N.i32ptr(sb),
                                           nccl_id))
 
+    def shard_host(self, rank: int, world: int, tleaf_bounds, sleaf_bounds, allgather, allreduce):
+        """The same partition over a HOST transport: ``allgather(send) -> recv`` (numpy
+        float64, recv = every rank's send concatenated in rank order) and ``allreduce(buf)``
+        (in-place sum) are called for every collective of the sharded apply / GMRES."""
+        tb = np.ascontiguousarray(tleaf_bounds, dtype=np.int32)
+        sb = np.ascontiguousarray(sleaf_bounds, dtype=np.int32)
+        if tb.shape != (world + 1,) or sb.shape != (world + 1,):
+            raise ValueError("bounds must have world + 1 entries")
+
+        def _ag(send_p, recv_p, count, _user):
+            try:
+                send = np.ctypeslib.as_array(send_p, shape=(count,))
+                recv = np.ctypeslib.as_array(recv_p, shape=(world * count,))
+                recv[:] = np.asarray(allgather(send.copy()), dtype=np.float64).reshape(-1)
+                return 0
+            except BaseException:  # reported as a CUDA-side failure of the collective
+                return 1
+
+        def _ar(buf_p, count, _user):
+            try:
+                buf = np.ctypeslib.as_array(buf_p, shape=(count,))
+                buf[:] = np.asarray(allreduce(buf.copy()), dtype=np.float64).reshape(-1)
+                return 0
+            except BaseException:
+                return 1
+
+        # the ctypes thunks must outlive the shard
+        self._host_cbs = (N.ALLGATHER_CALLBACK(_ag), N.ALLREDUCE_CALLBACK(_ar))
+        N.check(self._lib.fmmbem_op_shard_host(self._h, int(rank), int(world), N.i32ptr(tb),
+                                               N.i32ptr(sb), self._host_cbs[0],
+                                               self._host_cbs[1], None))
+
     def unshard(self):
         N.check(self._lib.fmmbem_op_unshard(self._h))
+        self._host_cbs = None
 
     def owned_panels(self, tleaf_bounds, rank: int) -> np.ndarray:
         """Panel indices whose rows rank `rank` computes under the given target split."""

@@ -1,9 +1,15 @@
 """Multi-GPU host logic: one process per GPU (torch.distributed for the plumbing).
 
-Round-1 scope: ``bench.py`` runs N independent replicas (one per GPU) and
-reduces device times as max over ranks; the partitioned solve (target leaves
-split across GPUs, NCCL all-gather of source multipoles, all-reduce of the
-Arnoldi dots) builds on ``partition_contiguous`` below.
+The partitioned solve (csrc/shard.cu + csrc/gmres.cu): the target leaves and
+the source leaves are split into contiguous, work-balanced ranges (``partition_contiguous``);
+each rank does the P2M of its source leaves, all-gathers the leaf multipoles, and runs M2L /
+P2P / the epilogue for its own target leaves.  GMRES keeps only each rank's rows of the
+Krylov vectors: v_k is all-gathered before every apply and the Gram-Schmidt dot products are
+all-reduced (CGS2).  The collectives go over NCCL (``shard_operator(..., transport="nccl")``,
+one GPU per rank, captured in the per-order CUDA graphs) or over a host transport
+(``transport="gloo"``: torch.distributed on CPU tensors behind the C callbacks; used to run
+two ranks on one GPU in the tests).  Multi-GPU timings: unmeasured on hardware (no multi-GPU
+node in this build's runs).
 """
 
 from __future__ import annotations
@@ -61,14 +67,40 @@ def broadcast_bytes(data: bytes | None, src: int = 0) -> bytes:
     return obj[0]
 
 
-def shard_operator(op, rank: int, world: int):
-    """Partition op's work over the torch.distributed world (one GPU per rank).
+def gloo_collectives(world: int):
+    """(allgather, allreduce) on host float64 arrays over the current torch.distributed group."""
+    import torch
+    import torch.distributed as dist
 
-    Every rank computes the same bounds; rank 0 creates the NCCL id and shares it.
+    def allgather(send):
+        t = torch.from_numpy(send)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return torch.cat(out).numpy()
+
+    def allreduce(buf):
+        t = torch.from_numpy(buf)
+        dist.all_reduce(t)
+        return t.numpy()
+
+    return allgather, allreduce
+
+
+def shard_operator(op, rank: int, world: int, transport: str = "nccl"):
+    """Partition op's work over the torch.distributed world.
+
+    Every rank computes the same bounds.  transport "nccl": one GPU per rank, rank 0 creates
+    the NCCL id and shares it; "gloo": the collectives run on host buffers through
+    torch.distributed (any backend), e.g. several ranks sharing one GPU.
     """
     tb, sb = leaf_bounds(op, world)
-    uid = broadcast_bytes(nccl_unique_id() if rank == 0 else None)
-    op.shard(rank, world, tb, sb, uid)
+    if transport == "nccl":
+        uid = broadcast_bytes(nccl_unique_id() if rank == 0 else None)
+        op.shard(rank, world, tb, sb, uid)
+    elif transport == "gloo":
+        op.shard_host(rank, world, tb, sb, *gloo_collectives(world))
+    else:
+        raise ValueError(f"unknown transport {transport!r}")
     return tb, sb
 
 

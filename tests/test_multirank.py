@@ -95,3 +95,39 @@ def test_two_rank_nccl_id_broadcast():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(r[1] == bytes(range(128)) for r in res)
+
+
+def _gloo_collectives_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_1506_05957_b200.parallel import gloo_collectives
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ag, ar = gloo_collectives(world)
+        send = np.arange(5, dtype=np.float64) + 10.0 * rank
+        out.put((rank, ag(send.copy()).tolist(), ar(send.copy()).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_transport_collectives_over_gloo():
+    """The (allgather, allreduce) pair the host transport of a sharded operator calls
+    (parallel.gloo_collectives -> fmmbem_op_shard_host): rank-ordered gather, in-place sum."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_collectives_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want_g = list(np.arange(5.0)) + list(np.arange(5.0) + 10.0)
+    want_r = list(2 * np.arange(5.0) + 10.0)
+    for _, g, r in res:
+        assert g == want_g and r == want_r
