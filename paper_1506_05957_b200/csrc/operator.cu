@@ -690,7 +690,15 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);
     record(op, ST_DOWN, false, s);
-    if (l2l_rot_mode(op, c.p, sharded, c.dense)) launch_l2l_rot(pl, c.p, C, op.L.get(), s);
+    if (l2l_rot_mode(op, c.p, sharded, c.dense)) {
+      // the L2L levels hold few cells each: the dense one-CTA-per-cell kernel has the shorter
+      // critical path (FMMBEM_L2L=rot: the DMMA rotation kernel, one warp per 8 cells)
+      static const bool rot = std::getenv("FMMBEM_L2L") && std::string(std::getenv("FMMBEM_L2L")) == "rot";
+      if (rot)
+        launch_l2l_rot(pl, c.p, C, op.L.get(), s);
+      else
+        launch_l2l(pl.tgt, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
+    }
     record(op, ST_DOWN, true, s);
   }
   if (!serial) FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
