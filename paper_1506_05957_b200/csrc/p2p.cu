@@ -620,6 +620,12 @@ void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const dou
   auto kern = nstg == 3 ? k_p2p_lapd<LAPD_CONS, 3> : k_p2p_lapd<LAPD_CONS, 2>;
   const int nthr = LAPD_CONS + LAPD_PROD;
   FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // shared-memory carveout of the SMs this persistent kernel occupies: the far-field kernels
+  // launched beside it can only co-reside in what the configuration leaves over
+  // (FMMBEM_P2P_CARVEOUT=percent, -1 = driver default)
+  static const int carve = std::getenv("FMMBEM_P2P_CARVEOUT") ? std::atoi(std::getenv("FMMBEM_P2P_CARVEOUT")) : -1;
+  if (carve >= 0)
+    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
   int dev = 0, sms = 0;
   FMM_CUDA(cudaGetDevice(&dev));
   FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
