@@ -112,6 +112,8 @@ def test_cfg4_relaxed_gmres_matches_reference():
     np.testing.assert_allclose(res.residuals[:k], g["relaxed_residuals"][:k], rtol=1e-5)
     assert rel_l2(res.x[g["rows"]], g["relaxed_x_rows"]) <= 1e-6
     assert abs(np.linalg.norm(res.x) / float(g["relaxed_x_norm"]) - 1.0) <= 1e-6
+    drag = op.drag_force(res.x)
+    assert np.linalg.norm(drag - g["drag"]) <= 1e-6 * np.linalg.norm(g["drag"])
 
 
 @pytest.mark.parametrize("name", ["cfg2", "cfg3"])

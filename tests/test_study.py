@@ -65,3 +65,48 @@ def test_convergence_sequence_on_device():
     assert all(r["converged"] for r in rep.records)
     assert err[0] > err[1] > err[2]
     assert np.isfinite(rep.derived["order"]) and rep.derived["order"] > 0.5
+
+
+def _study_golden():
+    import json
+
+    from conftest import load_golden
+
+    g = load_golden("study")
+    return g, json
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("problem,kw", [
+    ("laplace2", dict(level=3, tol=1e-6, p_initial=10, p_min=3, ncrit_candidates=(16, 64))),
+    ("stokes", dict(level=2, tol=1e-5, p_initial=12, p_min=5, ncrit_candidates=(16, 64)))])
+def test_relaxation_comparison_matches_the_reference(problem, kw):
+    """Same records as the reference's run_relaxation_comparison (study.py:207-242, run by
+    tools/make_goldens_study.py): per (n_crit, relaxed) the panel count, the iteration count
+    (+-1) and convergence; wall times are machine properties and are not compared."""
+    from paper_1506_05957_b200.study import run_relaxation_comparison
+
+    g, json = _study_golden()
+    want = json.loads(str(g[f"relax_{problem}_records"]))
+    rep = run_relaxation_comparison(problem, repeats=1, warmup=0, **kw)
+    got = [{k: r[k] for k in ("N", "n_crit", "relaxed", "iterations", "converged")} for r in rep.records]
+    assert len(got) == len(want)
+    for a, b in zip(got, want):
+        assert (a["N"], a["n_crit"], a["relaxed"], a["converged"]) == \
+               (b["N"], b["n_crit"], b["relaxed"], b["converged"])
+        assert abs(a["iterations"] - b["iterations"]) <= 1, (a, b)
+
+
+@pytest.mark.gpu
+def test_convergence_study_matches_the_reference():
+    """run_convergence (study.py:143-191) on the same refinement sequence: panel counts,
+    iterations and orders equal, errors to 1e-6 relative, the observed order to 1e-5."""
+    from paper_1506_05957_b200.study import run_convergence
+
+    g, json = _study_golden()
+    want = json.loads(str(g["conv_laplace2_records"]))
+    rep = run_convergence("laplace2", levels=[1, 2, 3], p=10, tol=1e-8, n_crit=32, p_min=3)
+    for a, b in zip(rep.records, want):
+        assert (a["N"], a["iterations"], list(a["orders"])) == (b["N"], b["iterations"], b["orders"])
+        assert abs(a["error"] - b["error"]) <= 1e-6 * b["error"]
+    assert abs(rep.derived["order"] - float(g["conv_laplace2_order"])) <= 1e-5
