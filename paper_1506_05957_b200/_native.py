@@ -147,6 +147,20 @@ def f64(a, shape=None) -> np.ndarray:
     return out
 
 
+def host_array(n: int) -> np.ndarray:
+    """A new float64 host array for a result the device writes: page-locked (torch's caching
+    host allocator: no first-touch page faults, the D2H copy lands in it directly) when a
+    CUDA torch is importable, else plain numpy."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    except Exception:
+        pass
+    return np.empty(n)
+
+
 def device_count() -> int:
     n = ctypes.c_int32(0)
     check(load().fmmbem_device_count(ctypes.byref(n)))

@@ -431,17 +431,22 @@ int fmmbem_op_gmres(fmmbem_op* h, const double* b, double tol, double eta, int p
     FMM_CUDA(cudaMemcpyAsync(op.stage_x.get(), b, op.n * sizeof(double), cudaMemcpyHostToDevice, op.s_main));
     gmres_common(h, op.stage_x.get(), tol, eta, p_initial, p_min, relaxed, max_iter,
                  op.stage_y.get(), residuals, orders, n_iter, converged, cb, user);
-    // x through a pinned staging buffer (a pageable D2H copy is staged by the driver, slower)
-    if (op.xpin_cap < op.n) {
+    // x straight into the caller's buffer when it is page-locked (the Python wrapper hands
+    // out pinned arrays), else through a pinned staging buffer (a pageable D2H copy is
+    // staged by the driver, slower)
+    cudaPointerAttributes pa{};
+    const bool x_pinned = cudaPointerGetAttributes(&pa, x) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    if (!x_pinned) cudaGetLastError();
+    if (!x_pinned && op.xpin_cap < op.n) {
       if (op.xpin_h) FMM_CUDA(cudaFreeHost(op.xpin_h));
       FMM_CUDA(cudaHostAlloc(&op.xpin_h, op.n * sizeof(double), cudaHostAllocDefault));
       op.xpin_cap = op.n;
     }
-    FMM_CUDA(cudaMemcpyAsync(op.xpin_h, op.stage_y.get(), op.n * sizeof(double), cudaMemcpyDeviceToHost,
-                             op.s_main));
+    FMM_CUDA(cudaMemcpyAsync(x_pinned ? x : op.xpin_h, op.stage_y.get(), op.n * sizeof(double),
+                             cudaMemcpyDeviceToHost, op.s_main));
     FMM_CUDA(cudaEventRecord(op.call_ev[1], op.s_main));
     FMM_CUDA(cudaStreamSynchronize(op.s_main));
-    std::memcpy(x, op.xpin_h, op.n * sizeof(double));
+    if (!x_pinned) std::memcpy(x, op.xpin_h, op.n * sizeof(double));
     float ms = 0.f;
     FMM_CUDA(cudaEventElapsedTime(&ms, op.call_ev[0], op.call_ev[1]));
     op.last_call_ms = ms;

@@ -356,6 +356,85 @@ void launch_epilogue(BemOp& op, const EpiArgs& a, bool far, cudaStream_t s, int 
   FMM_LAUNCH_CHECK();
 }
 
+
+// Far part of the one-channel epilogue when each leaf holds its complete local expansion (the
+// L2L mode): one thread per target, the whole L2P of the leaf's expansion (harmonics.py:
+// 258-270), y[panel] += beta phi / (4 pi).  Fully unrolled for the order P, so the columns'
+// n-recurrences (serial within a column) interleave across columns; the leaf's expansion is
+// staged once per CTA.  Replaces the path-walk epilogue's 4 column slices, whose lanes sat
+// idle on the ~80-target leaves of cfg5.
+constexpr int L2PL_THREADS = 128;
+
+template <int P>
+__global__ void __launch_bounds__(L2PL_THREADS) k_leaf_l2p(TreeDev T, const int* __restrict__ leaves,
+                                                           const int* __restrict__ has_far,
+                                                           const double2* __restrict__ L, double beta,
+                                                           double* __restrict__ y, double* __restrict__ ysorted,
+                                                           int tbody_a) {
+  constexpr int H = hcount(P);
+  __shared__ double2 sL[H];
+  const int leaf = leaves[blockIdx.x];
+  if (has_far[leaf + 1] == has_far[leaf]) return;  // no local expansion reaches this leaf
+  const int nt = T.body_count[leaf];
+  const int lt = blockIdx.y * L2PL_THREADS + threadIdx.x;
+  if ((int)blockIdx.y * L2PL_THREADS >= nt) return;
+  pdl_wait();  // L (the L2L levels) is complete past this point
+  for (int i = threadIdx.x; i < H; i += L2PL_THREADS) sL[i] = L[(size_t)leaf * H + i];
+  __syncthreads();
+  if (lt >= nt) return;
+  const int ti = T.body_start[leaf] + lt;
+  const double x = T.px[ti] - T.cx[leaf], yy = T.py[ti] - T.cy[leaf], z = T.pz[ti] - T.cz[leaf];
+  const double rho2 = x * x + yy * yy + z * z;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // independent partial sums (m mod 4)
+  double2 diag = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int m = 0; m <= P; ++m) {
+    if (m > 0) diag = cscale(cmul(make_double2(x, yy), diag), -1.0 / (2.0 * m));  // R_m^m (harmonics.py:50-52)
+    double2 cur = diag, prev2 = make_double2(0.0, 0.0);
+    int i = hidx(m, m);
+    double col = fma(sL[i].x, cur.x, -sL[i].y * cur.y);
+#pragma unroll
+    for (int n = m + 1; n <= P; ++n) {
+      double2 nx;
+      if (n == m + 1) {
+        nx = cscale(cur, z);
+      } else {
+        const double az = c_l2p.ra[n * (P_MAX + 1) + m] * z, b = c_l2p.rb[n * (P_MAX + 1) + m] * rho2;
+        nx = make_double2(fma(az, cur.x, -b * prev2.x), fma(az, cur.y, -b * prev2.y));
+      }
+      prev2 = cur;
+      cur = nx;
+      i += n;
+      col = fma(sL[i].x, cur.x, fma(-sL[i].y, cur.y, col));
+    }
+    acc[m & 3] = m == 0 ? acc[0] + col : fma(2.0, col, acc[m & 3]);
+  }
+  const double phi = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  double* dst = ysorted ? ysorted + (ti - tbody_a) : y + T.perm[ti];
+  *dst += beta * (phi / FOUR_PI);
+}
+
+template <int P>
+void launch_leaf_l2p_p(BemOp& op, const double* L, double beta, double* y, cudaStream_t s) {
+  const Tree& T = op.plan.tgt;
+  const int tiles = (std::max(T.max_leaf_count, 1) + L2PL_THREADS - 1) / L2PL_THREADS;
+  if (T.n_leaves > 0)
+    launch_pdl(k_leaf_l2p<P>, dim3(T.n_leaves, tiles), dim3(L2PL_THREADS), 0, s, tree_dev(T),
+               (const int*)T.leaves.get(), (const int*)op.plan.epi_leaf_off.get(),
+               reinterpret_cast<const double2*>(L), beta, y, (double*)nullptr, 0);
+  FMM_LAUNCH_CHECK();
+}
+
+template <int... Ps>
+void launch_leaf_l2p(std::integer_sequence<int, Ps...>, int p, BemOp& op, const double2* L,
+                     double beta, double* y, cudaStream_t s) {
+  bool done = false;
+  ((p == Ps && !done ? (launch_leaf_l2p_p<Ps>(op, reinterpret_cast<const double*>(L), beta, y, s), done = true)
+                     : false),
+   ...);
+  FMM_REQUIRE(done, "leaf L2P: order out of range");
+}
+
 int layer_channels(int kind) { return kind == K_STOKESLET ? 4 : kind == K_STRESSLET ? 7 : 1; }
 
 void ensure_dense(BemOp& op) {
@@ -600,6 +679,10 @@ void launch_layer_epilogue(BemOp& op, const LayerCall& c, bool sharded, cudaStre
     FMM_LAUNCH_CHECK();
     return;
   }
+  if (mode == 2 && l2l && (c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE) && !a.ysorted) {
+    launch_leaf_l2p(std::make_integer_sequence<int, P_MAX + 1>{}, c.p, op, op.L.get(), c.beta, c.y, s);
+    return;
+  }
   switch (c.kind) {
     case K_LAP_SINGLE: launch_epilogue<K_LAP_SINGLE>(op, a, far, s, n_epi); break;
     case K_LAP_DOUBLE: launch_epilogue<K_LAP_DOUBLE>(op, a, far, s, n_epi); break;
@@ -630,6 +713,46 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   }
   const double* w = c.kind == K_LAP_SINGLE ? op.q.get() : c.kind == K_LAP_DOUBLE ? op.dip.get()
                                                                                 : op.wsrc.get();
+  // far-field stages as steps; FMMBEM_AHEAD=1 (upward) / 2 (upward + M2L) issues them before
+  // the near field is forked (scheduling experiments; default 0: all after the fork)
+  auto upward = [&]() {
+    const double* q = (c.kind == K_LAP_SINGLE || c.kind == K_STOKESLET) ? op.q.get() : nullptr;
+    const double* d = (c.kind == K_LAP_DOUBLE || c.kind == K_STRESSLET) ? op.dip.get() : nullptr;
+    record(op, ST_UP, false, s);
+    const bool own_only = sharded && !sw.virtual_mode;  // P2M of own leaves, then all-gather
+    const int* lv = own_only ? sw.p2m_leaves.get() : pl.src.leaves.get();
+    const int nlv = own_only ? sw.n_p2m_leaves : pl.src.n_leaves;
+    const bool basis = c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p;
+    if (basis && op.basis_clustered && !own_only) {
+      // every multipole straight from the sources (no M2M levels), or the leaves' multipoles
+      // and the M2M chain above them
+      launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, nullptr, 0);
+      if (op.basis_leaf_only)
+        launch_upward_m2m(op, c.p, C, s);
+    } else {
+      if (basis)
+        launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, lv, nlv);
+      else
+        launch_p2m(S, lv, nlv, c.p, C, q, d, op.M.get(), s);
+      if (own_only) shard_exchange_multipoles(op, C, c.p, s);
+      launch_upward_m2m(op, c.p, C, s);
+    }
+    record(op, ST_UP, true, s);
+  };
+  auto m2l = [&]() {
+    record(op, ST_M2L, false, s);
+    if (sharded)
+      launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s, sw.gitems.get(),
+                 (int)sw.gitems_h.size(), sw.gather_cells.get(), sw.n_gather_cells, sw.gpair.get(),
+                 sw.citems.get(), sw.n_citems, sw.cpair.get());
+    else
+      launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
+    record(op, ST_M2L, true, s);
+  };
+  static const int ahead_env = std::getenv("FMMBEM_AHEAD") ? std::atoi(std::getenv("FMMBEM_AHEAD")) : 0;
+  const int ahead = c.dense ? 0 : ahead_env;
+  if (ahead >= 1) upward();
+  if (ahead >= 2) m2l();
   // near field on the second stream
   // near field on the second stream (concurrent with the far field), or in line
   const bool serial = op.serial_near;
@@ -659,36 +782,9 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   if (!serial) FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
   // far field on the main stream
   if (!c.dense) {
-    const double* q = (c.kind == K_LAP_SINGLE || c.kind == K_STOKESLET) ? op.q.get() : nullptr;
-    const double* d = (c.kind == K_LAP_DOUBLE || c.kind == K_STRESSLET) ? op.dip.get() : nullptr;
-    record(op, ST_UP, false, s);
-    const bool own_only = sharded && !sw.virtual_mode;  // P2M of own leaves, then all-gather
-    const int* lv = own_only ? sw.p2m_leaves.get() : pl.src.leaves.get();
-    const int nlv = own_only ? sw.n_p2m_leaves : pl.src.n_leaves;
-    const bool basis = c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p;
-    if (basis && op.basis_clustered && !own_only) {
-      // every multipole straight from the sources (no M2M levels), or the leaves' multipoles
-      // and the M2M chain above them
-      launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, nullptr, 0);
-      if (op.basis_leaf_only)
-        launch_upward_m2m(op, c.p, C, s);
-    } else {
-      if (basis)
-        launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, lv, nlv);
-      else
-        launch_p2m(S, lv, nlv, c.p, C, q, d, op.M.get(), s);
-      if (own_only) shard_exchange_multipoles(op, C, c.p, s);
-      launch_upward_m2m(op, c.p, C, s);
-    }
-    record(op, ST_UP, true, s);
-    record(op, ST_M2L, false, s);
-    if (sharded)
-      launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s, sw.gitems.get(),
-                 (int)sw.gitems_h.size(), sw.gather_cells.get(), sw.n_gather_cells, sw.gpair.get(),
-                 sw.citems.get(), sw.n_citems, sw.cpair.get());
-    else
-      launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
-    record(op, ST_M2L, true, s);
+    if (ahead < 1) upward();
+    if (ahead < 2) m2l();
+
     record(op, ST_DOWN, false, s);
     if (l2l_rot_mode(op, c.p, sharded, c.dense)) {
       // the L2L levels hold few cells each: the dense one-CTA-per-cell kernel has the shorter

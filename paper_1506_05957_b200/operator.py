@@ -285,7 +285,7 @@ class GpuBemOperator:
     def apply(self, x, p=12):
         """System mat-vec A x with expansions truncated at order p (bemop.py:272-274)."""
         v = self._vec(x)
-        y = np.empty(self._n)
+        y = N.host_array(self._n)
         N.check(self._lib.fmmbem_op_apply(self._h, N.dptr(v), N.dptr(y), int(p)))
         return y
 

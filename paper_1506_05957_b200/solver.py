@@ -71,7 +71,7 @@ def _device_gmres(op, b, schedule, tol, max_iter, callback=None):
     lib = N.load()
     bb = op._vec(b)
     n = len(bb)
-    x = np.empty(n)
+    x = N.host_array(n)
     res = np.zeros(max(max_iter, 1))
     orders = np.zeros(max(max_iter, 1), dtype=np.int32)
     nit = ctypes.c_int32(0)
