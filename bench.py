@@ -505,6 +505,7 @@ def run_ours(args, cfg, mesh, world):
         "wall_s_timed_region": wall,
         "e2e": {"value": e2e_value, "unit": "matvecs/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e2e_ms)),
+                "ms_median": float(np.median(e2e_ms)), "ms_max": float(np.max(e2e_ms)),
                 "api": "paper_1506_05957_b200.solver (fmmbem_op_gmres), host pinned b, host x"},
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 LIB_NAME = "libfmmbem_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# FMMBEM_LIB: an alternative build of the same library (A/B kernel experiments, tools/)
+LIB_PATH = os.environ.get("FMMBEM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 _c_double_p = ctypes.POINTER(ctypes.c_double)
 _c_int64_p = ctypes.POINTER(ctypes.c_int64)

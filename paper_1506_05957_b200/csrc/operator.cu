@@ -526,6 +526,16 @@ void prepare(BemOp& op, int kind, int p, bool dense) {
   }
 }
 
+bool timeline_on() {
+  static const bool on = std::getenv("FMMBEM_TIMELINE") != nullptr;
+  return on;
+}
+
+void mark(BemOp& op, int i, cudaStream_t s) {
+  if (op.timing && timeline_on())
+    FMM_CUDA(cudaEventRecordWithFlags(op.ev_tl[i], s, cudaEventRecordExternal));
+}
+
 void record(BemOp& op, int stage, bool end, cudaStream_t s) {
   // External: inside a stream capture this becomes a real event-record node
   if (op.timing)
@@ -541,6 +551,8 @@ BemOp::~BemOp() {
   if (ypin_h) cudaFreeHost(ypin_h);
   if (mflag_h) cudaFreeHost(mflag_h);
   for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ev_tl)
     if (e) cudaEventDestroy(e);
   for (auto& e : call_ev)
     if (e) cudaEventDestroy(e);
@@ -580,6 +592,7 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_enter, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_leave, cudaEventDisableTiming));
   for (auto& e : op.ev) FMM_CUDA(cudaEventCreate(&e));
+  for (auto& e : op.ev_tl) FMM_CUDA(cudaEventCreate(&e));
   for (auto& e : op.call_ev) FMM_CUDA(cudaEventCreate(&e));
   cudaStream_t s = op.s_main;
   // collocation points are bitwise the centroid Gauss point (bemop.py:64-67)
@@ -698,6 +711,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   const int C = layer_channels(c.kind);
   const TreeDev S = tree_dev(pl.src), T = tree_dev(pl.tgt);
   record(op, ST_TOTAL, false, s);
+  mark(op, 0, s);
   // the double layer's persistent near field reads x through static source records and the
   // basis upward pass reads x directly: the Gauss-point densities are only needed otherwise
   const bool basis_up = c.kind == op.basis_kind_for_sys && op.use_basis && op.basis_p >= c.p;
@@ -727,8 +741,10 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
       // every multipole straight from the sources (no M2M levels), or the leaves' multipoles
       // and the M2M chain above them
       launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, nullptr, 0);
+      mark(op, 1, s);
       if (op.basis_leaf_only)
         launch_upward_m2m(op, c.p, C, s);
+      mark(op, 2, s);
     } else {
       if (basis)
         launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, lv, nlv);
@@ -748,6 +764,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     else
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);
+    mark(op, 3, s);
   };
   static const int ahead_env = std::getenv("FMMBEM_AHEAD") ? std::atoi(std::getenv("FMMBEM_AHEAD")) : 0;
   const int ahead = c.dense ? 0 : ahead_env;
@@ -777,6 +794,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   // one-channel kinds: the near part of the epilogue (item partials + correction rows) runs
   // right behind the near field, concurrently with the far field
   record(op, ST_P2P, true, sn);
+  mark(op, 5, sn);
   const bool split_epi = !c.dense && (c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE || c.kind == K_STOKESLET);
   if (split_epi) launch_layer_epilogue(op, c, sharded, sn, 1);
   if (!serial) FMM_CUDA(cudaEventRecord(op.ev_join, op.s_near));
@@ -796,6 +814,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
         launch_l2l(pl.tgt, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
     }
     record(op, ST_DOWN, true, s);
+    mark(op, 4, s);
   }
   if (!serial) FMM_CUDA(cudaStreamWaitEvent(s, op.ev_join, 0));
   launch_layer_epilogue(op, c, sharded, s, split_epi ? 2 : 0);
@@ -804,6 +823,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     shard_exchange_y(op, c.kind == K_LAP_SINGLE || c.kind == K_LAP_DOUBLE ? 1 : 3, c.y, s);
   record(op, ST_EPI, true, s);
   record(op, ST_TOTAL, true, s);
+  mark(op, 6, s);
 }
 
 namespace {
@@ -821,6 +841,16 @@ void sys_call(BemOp& op, int p, bool dense, const double* x, double* y, LayerCal
 
 void accumulate_stage_times(BemOp& op) {
   if (!op.timing) return;
+  if (timeline_on()) {
+    float t[7];
+    for (int i = 0; i < 7; ++i)
+      if (cudaEventElapsedTime(&t[i], op.ev_tl[0], op.ev_tl[i]) != cudaSuccess) {
+        cudaGetLastError();
+        t[i] = -1.f;
+      }
+    std::fprintf(stderr, "TIMELINE basis %.3f m2m %.3f m2l %.3f l2l %.3f p2p %.3f end %.3f\n", t[1], t[2],
+                 t[3], t[4], t[5], t[6]);
+  }
   for (int st = 0; st < N_STAGES; ++st) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, op.ev[2 * st], op.ev[2 * st + 1]) == cudaSuccess)

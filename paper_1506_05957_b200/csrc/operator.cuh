@@ -181,6 +181,9 @@ struct BemOp {
   // stage timing
   bool timing = false;
   cudaEvent_t ev[2 * N_STAGES] = {};
+  // FMMBEM_TIMELINE=1 (with timing on): marks inside the apply, printed per apply to stderr
+  // (0 start, 1 basis stream done, 2 M2M done, 3 M2L done, 4 L2L done, 5 P2P done, 6 end)
+  cudaEvent_t ev_tl[8] = {};
   double stage_ms[N_STAGES] = {};
   int64_t stage_calls = 0;
 

@@ -209,6 +209,9 @@ k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __rest
 constexpr int LAPD_TPT = 4;
 constexpr int LAPD_CONS = 256;
 constexpr int LAPD_PROD = 128;
+#ifndef LAPD_SPT
+#define LAPD_SPT 2  // sources per trip of the consumer loop (tools: -DLAPD_SPT=3)
+#endif
 #ifndef LAPD_SPR
 #define LAPD_SPR 4
 #endif
@@ -487,6 +490,18 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
       for (; j < nspec; j += G) lapd_body<TPT, true>(lapd_load(sh2, max_src, j), j, tx, ty, tz, tt, self, acc);
       // software-pipelined: the next source's tile entry is read while this one is used
       if (j < ns) {
+#if LAPD_SPT == 3
+        // three sources per trip: 3 TPT independent chains in flight
+        for (; j + 2 * G < ns; j += 3 * G) {
+          const LapdSrc u = lapd_load(sh2, max_src, j);
+          const LapdSrc v = lapd_load(sh2, max_src, j + G);
+          const LapdSrc w2 = lapd_load(sh2, max_src, j + 2 * G);
+          lapd_body<TPT, false>(u, j, tx, ty, tz, tt, self, acc);
+          lapd_body<TPT, false>(v, j + G, tx, ty, tz, tt, self, acc);
+          lapd_body<TPT, false>(w2, j + 2 * G, tx, ty, tz, tt, self, acc);
+        }
+        for (; j < ns; j += G) lapd_body<TPT, false>(lapd_load(sh2, max_src, j), j, tx, ty, tz, tt, self, acc);
+#else
         LapdSrc u = lapd_load(sh2, max_src, j);
         for (; j + G < ns; j += 2 * G) {
           // two sources per trip: 2 TPT independent chains in flight
@@ -497,6 +512,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
           u = w2;
         }
         if (j < ns) lapd_body<TPT, false>(u, j, tx, ty, tz, tt, self, acc);
+#endif
       }
     }
     if (threadIdx.x == 0) TR(k, 5);

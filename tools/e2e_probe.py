@@ -53,3 +53,18 @@ t = time.perf_counter()
 for _ in range(10):
     v = op._vec(bp)
 print('_vec ms', (time.perf_counter() - t) * 100)
+# the bench's e2e loop: L2 flush + sync before every timed call
+flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+walls, evs = [], []
+for _ in range(10):
+    flush.zero_()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    out = _device_gmres(op, bp, sched, cfg.tol, cfg.max_iter)
+    walls.append(time.perf_counter() - t)
+    evs.append(op.counters()[2])
+print('bench-style e2e: wall ms', np.median(walls) * 1e3, 'mean', np.mean(walls) * 1e3, 'event ms', np.median(evs))
+t = time.perf_counter()
+for _ in range(10):
+    a = N.host_array(op.shape[0])
+print('host_array ms', (time.perf_counter() - t) * 100)
