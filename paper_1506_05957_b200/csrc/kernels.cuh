@@ -47,6 +47,7 @@ void build_rot_frag(const double* rot, int n_off, int P, double* out, cudaStream
 void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
                     int C, const double2* M, double2* pout, cudaStream_t st, bool cls);
 constexpr int M2L_ROT_MIN_P = 3;  // rotation-based M2L from this order up
+void launch_m2l_gather(const Plan& plan, int p, int C, const double2* part, double2* L, cudaStream_t st);
 // M2M by rotation (point and shoot, DMMA): per-child contributions into cout, then the
 // children of every parent summed in order (p >= M2L_ROT_MIN_P; plan_ensure_m2m_rot first)
 void launch_m2m_rot(const Plan& plan, int p, int C, double2* M, double2* cout, cudaStream_t st);

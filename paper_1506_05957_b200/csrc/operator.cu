@@ -559,6 +559,9 @@ BemOp::~BemOp() {
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   if (ev_enter) cudaEventDestroy(ev_enter);
+  if (ev_basis) cudaEventDestroy(ev_basis);
+  if (ev_m2l2) cudaEventDestroy(ev_m2l2);
+  if (s_far2) cudaStreamDestroy(s_far2);
   if (ev_leave) cudaEventDestroy(ev_leave);
   if (s_main) cudaStreamDestroy(s_main);
   if (s_near) cudaStreamDestroy(s_near);
@@ -590,6 +593,10 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_fork, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_join, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_enter, cudaEventDisableTiming));
+  // (low priority: the latency-bound M2M levels on s_main must not wait for the leaf M2L's CTAs)
+  FMM_CUDA(cudaStreamCreateWithPriority(&op.s_far2, cudaStreamNonBlocking, prio_lo));
+  FMM_CUDA(cudaEventCreateWithFlags(&op.ev_basis, cudaEventDisableTiming));
+  FMM_CUDA(cudaEventCreateWithFlags(&op.ev_m2l2, cudaEventDisableTiming));
   FMM_CUDA(cudaEventCreateWithFlags(&op.ev_leave, cudaEventDisableTiming));
   for (auto& e : op.ev) FMM_CUDA(cudaEventCreate(&e));
   for (auto& e : op.ev_tl) FMM_CUDA(cudaEventCreate(&e));
@@ -727,6 +734,26 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
   }
   const double* w = c.kind == K_LAP_SINGLE ? op.q.get() : c.kind == K_LAP_DOUBLE ? op.dip.get()
                                                                                 : op.wsrc.get();
+  // M2L split by source cell: the pairs with leaf sources run on a third stream as soon as the
+  // leaf basis stream is done, beside the (latency-bound) M2M levels; the rest after the M2M
+  // (FMMBEM_M2L_SPLIT=1; off by default: measured slower on cfg5, 445 vs 451 mat-vecs/s —
+  // the leaf M2L's long CTAs hold the SMs and each M2M level waits for slots, at any stream
+  // priority); the gather waits for both
+  static const bool split_env = std::getenv("FMMBEM_M2L_SPLIT") && std::string(std::getenv("FMMBEM_M2L_SPLIT")) == "1";
+  const bool split_m2l = split_env && !c.dense && !sharded && pl.use_rot && c.p >= M2L_ROT_MIN_P &&
+                         pl.rot_p >= c.p && !pl.m2l_ci_leaf.empty() &&
+                         !(op.basis_clustered && !op.basis_leaf_only && c.kind == op.basis_kind_for_sys &&
+                           op.use_basis && op.basis_p >= c.p);  // (direct basis: no M2M to hide)
+  bool leaf_m2l_forked = false;
+  auto fork_leaf_m2l = [&]() {
+    if (!split_m2l) return;
+    FMM_CUDA(cudaEventRecord(op.ev_basis, s));
+    FMM_CUDA(cudaStreamWaitEvent(op.s_far2, op.ev_basis, 0));
+    launch_m2l_rot(pl, pl.d_m2l_ci_leaf.get(), pl.m2l_cp_leaf.get(), (int)pl.m2l_ci_leaf.size(), c.p, C,
+                   op.M.get(), op.m2l_part.get(), op.s_far2, true);
+    FMM_CUDA(cudaEventRecord(op.ev_m2l2, op.s_far2));
+    leaf_m2l_forked = true;
+  };
   // far-field stages as steps; FMMBEM_AHEAD=1 (upward) / 2 (upward + M2L) issues them before
   // the near field is forked (scheduling experiments; default 0: all after the fork)
   auto upward = [&]() {
@@ -742,8 +769,10 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
       // and the M2M chain above them
       launch_p2m_basis(op, c.p, C, c.x, op.M.get(), s, nullptr, 0);
       mark(op, 1, s);
-      if (op.basis_leaf_only)
+      if (op.basis_leaf_only) {
+        fork_leaf_m2l();
         launch_upward_m2m(op, c.p, C, s);
+      }
       mark(op, 2, s);
     } else {
       if (basis)
@@ -751,13 +780,23 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
       else
         launch_p2m(S, lv, nlv, c.p, C, q, d, op.M.get(), s);
       if (own_only) shard_exchange_multipoles(op, C, c.p, s);
+      fork_leaf_m2l();
       launch_upward_m2m(op, c.p, C, s);
     }
     record(op, ST_UP, true, s);
   };
   auto m2l = [&]() {
     record(op, ST_M2L, false, s);
-    if (sharded)
+    if (split_m2l) {
+      launch_m2l_rot(pl, pl.d_m2l_ci_rest.get(), pl.m2l_cp_rest.get(), (int)pl.m2l_ci_rest.size(), c.p, C,
+                     op.M.get(), op.m2l_part.get(), s, true);
+      if (leaf_m2l_forked)
+        FMM_CUDA(cudaStreamWaitEvent(s, op.ev_m2l2, 0));
+      else  // (the upward path did not fork it)
+        launch_m2l_rot(pl, pl.d_m2l_ci_leaf.get(), pl.m2l_cp_leaf.get(), (int)pl.m2l_ci_leaf.size(), c.p, C,
+                       op.M.get(), op.m2l_part.get(), s, true);
+      launch_m2l_gather(pl, c.p, C, op.m2l_part.get(), op.L.get(), s);
+    } else if (sharded)
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s, sw.gitems.get(),
                  (int)sw.gitems_h.size(), sw.gather_cells.get(), sw.n_gather_cells, sw.gpair.get(),
                  sw.citems.get(), sw.n_citems, sw.cpair.get());

@@ -92,6 +92,9 @@ struct BemOp {
   cudaStream_t s_main = nullptr, s_near = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_enter = nullptr, ev_leave = nullptr;  // caller-stream ordering (capi.cu)
+  // third stream: the M2L of leaf sources beside the M2M levels (fork after the basis stream)
+  cudaStream_t s_far2 = nullptr;
+  cudaEvent_t ev_basis = nullptr, ev_m2l2 = nullptr;
 
   // geometry, panel order
   DevBuf<double> centroid, normal, area, panel_verts, gauss_pos, gauss_w, fine_pos, fine_w;

@@ -104,6 +104,11 @@ struct Plan {
   DevBuf<int4> d_m2l_citems;
   DevBuf<int> m2l_cpair;
   std::vector<int> h_m2l_cpair;
+  // the same class-grouped items split by source cell: leaf sources (their multipoles exist as
+  // soon as the leaf basis stream ends, so these run beside the M2M levels) and the rest
+  std::vector<int4> m2l_ci_leaf, m2l_ci_rest;
+  DevBuf<int4> d_m2l_ci_leaf, d_m2l_ci_rest;
+  DevBuf<int> m2l_cp_leaf, m2l_cp_rest;
   std::vector<int> m2l_tgt_cells;  // target cells with >= 1 M2L source
   DevBuf<int> d_m2l_tgt_cells;
 

@@ -620,6 +620,15 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
   FMM_LAUNCH_CHECK();
 }
 
+// L[cell] for every target cell from the per-pair slots (the second half of launch_m2l)
+void launch_m2l_gather(const Plan& plan, int p, int C, const double2* part, double2* L, cudaStream_t st) {
+  const int CH = C * hcount(p);
+  dim3 grid(plan.tgt.n_cells, (CH + 63) / 64);
+  if (plan.tgt.n_cells > 0)
+    launch_pdl(k_m2l_gather, grid, dim3(256), 0, st, (const int*)nullptr, plan.m2l_row.get(), CH, part, L);
+  FMM_LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------------------ M2M, octant-grouped
 // Children at one level that sit in the same octant of their parents share
 // R(d): one CTA per (level, octant, <= 8 children) applies it to 4 child

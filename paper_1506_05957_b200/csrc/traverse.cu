@@ -269,6 +269,34 @@ void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
     plan.h_m2l_cpair = gp;
     plan.d_m2l_citems.upload(plan.m2l_citems, s);
     plan.m2l_cpair.upload(gp, s);
+    {
+      std::vector<int> cpl, cpr;
+      plan.m2l_ci_leaf.clear();
+      plan.m2l_ci_rest.clear();
+      auto cut = [&](std::vector<int>& cp, std::vector<int4>& items, size_t start) {
+        const int len = (int)(cp.size() - start), nch = (len + 7) / 8;
+        for (int q = 0; q < nch; ++q) {
+          const int lo = (int)start + (int)((int64_t)len * q / nch);
+          const int hi = (int)start + (int)((int64_t)len * (q + 1) / nch);
+          items.push_back(make_int4(plan.h_m2l_off[cp[lo]], lo, hi, 0));
+        }
+      };
+      for (size_t i = 0; i < gp.size();) {
+        size_t j = i;
+        const int c0 = cls_of[plan.h_m2l_off[gp[i]]];
+        while (j < gp.size() && cls_of[plan.h_m2l_off[gp[j]]] == c0) ++j;
+        const size_t sl = cpl.size(), sr = cpr.size();
+        for (size_t k = i; k < j; ++k)
+          (plan.src.h_n_child[plan.h_m2l_src[gp[k]]] == 0 ? cpl : cpr).push_back(gp[k]);
+        cut(cpl, plan.m2l_ci_leaf, sl);
+        cut(cpr, plan.m2l_ci_rest, sr);
+        i = j;
+      }
+      plan.d_m2l_ci_leaf.upload(plan.m2l_ci_leaf.empty() ? std::vector<int4>(1) : plan.m2l_ci_leaf, s);
+      plan.d_m2l_ci_rest.upload(plan.m2l_ci_rest.empty() ? std::vector<int4>(1) : plan.m2l_ci_rest, s);
+      plan.m2l_cp_leaf.upload(cpl.empty() ? std::vector<int>(1, 0) : cpl, s);
+      plan.m2l_cp_rest.upload(cpr.empty() ? std::vector<int>(1, 0) : cpr, s);
+    }
   }
 
   plan.rotf.resize((size_t)nd * rot_frag_size(p));
