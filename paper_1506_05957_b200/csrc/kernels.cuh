@@ -73,15 +73,23 @@ inline int p2p_comps(P2PKind k) { return (k == P2PKind::LAP_Q || k == P2PKind::L
 // (start, count, tile offset) at their CSR position, and every item target's tile slot of
 // its own centroid Gauss point (-1 if not in the item) at its partial-sum position.
 struct LapdHdr {  // one P2P item in schedule (largest-first) order
-  int item, pair_begin, nl, ns, t0, nt, out_off, nspec;
-  double cx, cy, cz, pad2;  // target leaf centre
+  int pair_begin, nl, ns, t0, nt, out_off, nspec;
+  // tile sections: n1 single points (own sources first), n2 clusters of 2 and n3 clusters of 3
+  // points of one panel sharing the dipole term (ns = n1 + 2 n2 + 3 n3)
+  int n1, n2, n3;
+  double cx, cy, cz;  // target leaf centre
 };
 struct P2PAux {
   DevBuf<LapdHdr> hdr;
   int n_items = 0;
+  // per item source leaf: (body start, singles offset | pair-cluster offset << 16, tile offset,
+  // triple-cluster offset)
   DevBuf<int4> ltab;
   DevBuf<int> slot;  // per item target: its own source's tile slot (own sources first), or -1
-  DevBuf<int> spec;  // per item: the own sources' positions in item (leaf) order, ascending
+  DevBuf<int> spec;  // per item: the own sources' positions among the item's singles, ascending
+  // per sorted source: section (0 single, 1 pair, 2 triple) | position in its cluster << 2 |
+  // rank inside its leaf's section << 4
+  DevBuf<int> code;
   int max_leaves = 1, max_tgt = 1;
   bool ready = false;
   void build(const Tree& S, const Tree& T, const std::vector<P2PItem>& items,

@@ -17,6 +17,7 @@
 // instead of the reference's four-channel decomposition of the near field;
 // the two agree to ~1e-13 and the direct form is cheaper.
 #include <algorithm>
+#include <cstdio>
 
 #include "kernels.cuh"
 #include "l2p.cuh"
@@ -295,12 +296,78 @@ __device__ __forceinline__ void lapd_body(const LapdSrc& u, int j, const double*
   }
 }
 
+// Panel-shared dipole term.  The far rule's Gauss points of one panel lie in the panel's plane
+// and carry the same normal and density, so d.(t - y_j) = d.t' - d.s'_j is the same for every
+// point j of the panel (d.s'_j = d.s'_0 exactly for a flat panel), and the three outer points
+// share one weight (quadrature.py:47-52: -27/48 at the centroid, 25/48 at the others).  The
+// outer points of one panel inside one source leaf therefore form a cluster of C <= 3 points:
+//   sum_j d.(t - y_j) / r_j^3 = (d.(t - y_0)) * sum_j r_j^-3
+// costs 8 C + 4 DP instructions instead of 12 C.  The centroids and lone outer points stay
+// single points (12 instructions); measured on a synthetic tile (tools/p2p_cluster_probe.cu):
+// 32.4 (single) / 26.8 (C = 2) / 23.8 (C = 3) cycles per warp-interaction.
+template <int C>
+struct LapdCl {
+  double2 ab[C], cs[C], dxy, dzs;
+};
+
+template <int C>
+__device__ __forceinline__ LapdCl<C> lapd_load_cl(const double2* __restrict__ sh2, int max_src, int rec, int pt) {
+  LapdCl<C> u;
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    u.ab[i] = sh2[pt + i];
+    u.cs[i] = sh2[max_src + pt + i];
+  }
+  u.dxy = sh2[2 * max_src + rec];
+  u.dzs = sh2[3 * max_src + rec];
+  return u;
+}
+
+template <int TPT, int C>
+__device__ __forceinline__ void lapd_body_cl(const LapdCl<C>& u, const double* tx, const double* ty,
+                                             const double* tz, const double* tt, double* acc) {
+#pragma unroll
+  for (int q = 0; q < TPT; ++q) {
+    const double rn = fma(u.dxy.x, tx[q], fma(u.dxy.y, ty[q], fma(u.dzs.x, tz[q], u.dzs.y)));
+    double k = 0.0;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const double d2 = fma(tx[q], u.ab[i].x, fma(ty[q], u.ab[i].y, fma(tz[q], u.cs[i].x, u.cs[i].y + tt[q])));
+      double y;
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d2));
+      const double y2 = y * y;
+      const double g = fma(d2, y2, -5.0 / 3.0);
+      const double y3 = y2 * y;
+      k = i == 0 ? y3 * g : fma(y3, g, k);
+    }
+    acc[q] = fma(rn, k, acc[q]);
+  }
+}
+
+// the clusters of one tile section: records [rec0, rec0 + n), points from pt0 (C per cluster);
+// thread group g of G takes the records r = g (mod G), so the groups' shares stay balanced
+// across the sections; the next cluster is read while this one is used
+template <int TPT, int C>
+__device__ __forceinline__ void lapd_run_clusters(const double2* __restrict__ sh2, int max_src, int rec0, int pt0,
+                                                  int n, int g, int G, const double* tx, const double* ty,
+                                                  const double* tz, const double* tt, double* acc) {
+  int c = (g - rec0 % G + G) % G;
+  if (c >= n) return;
+  LapdCl<C> u = lapd_load_cl<C>(sh2, max_src, rec0 + c, pt0 + C * c);
+  for (; c + G < n; c += G) {
+    const LapdCl<C> v = lapd_load_cl<C>(sh2, max_src, rec0 + c + G, pt0 + C * (c + G));
+    lapd_body_cl<TPT, C>(u, tx, ty, tz, tt, acc);
+    u = v;
+  }
+  lapd_body_cl<TPT, C>(u, tx, ty, tz, tt, acc);
+}
+
 template <int NCT, int NSTG>
 __global__ void __launch_bounds__(NCT + LAPD_PROD, 1)
 k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4* __restrict__ gl_ltab,
            const int* __restrict__ gl_slot, const int* __restrict__ gl_spec, int max_src, int max_leaves, int max_tgt,
-           const double2* __restrict__ srec, const int* __restrict__ s_panel, const double* __restrict__ xd,
-           double* __restrict__ part, unsigned* __restrict__ sched,
+           const double2* __restrict__ srec, const int* __restrict__ s_panel, const int* __restrict__ s_code,
+           const double* __restrict__ xd, double* __restrict__ part, unsigned* __restrict__ sched,
            long long* __restrict__ trace) {
   constexpr int TPT = LAPD_TPT, NPT = LAPD_PROD, ALL = NCT + NPT;
   // optional per-item clock trace (FMMBEM_P2P_TRACE): [cta][item < 32][8]
@@ -325,7 +392,7 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
     int* slot = reinterpret_cast<int*>(base + L.slot);
     double2* tg = reinterpret_cast<double2*>(base + L.tgt);
     int* spec = slot + max_tgt;  // tile positions (item order) of the targets' own sources
-    int* hdr = spec + max_tgt;   // live (0: done), ns, nt, out_off, nspec
+    int* hdr = spec + max_tgt;   // live (0: done), ns, nt, out_off, nspec, n1, n2, n3
     if (cur >= n_items) {
       if (tid == 0) hdr[0] = 0;
       return false;
@@ -345,13 +412,16 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
       hdr[2] = H.nt;
       hdr[3] = H.out_off;
       hdr[4] = H.nspec;
+      hdr[5] = H.n1;
+      hdr[6] = H.n2;
+      hdr[7] = H.n3;
     }
     if (all) __syncthreads();
     else bar_sync(BAR_PROD, NPT);
     // flattened over the tile: SPR sources per thread per round, loads issued before use
     for (int i0 = tid; i0 < H.ns; i0 += SPR * nthr) {
       double2 v[SPR][3];
-      int pn[SPR];
+      int pn[SPR], cd[SPR], o12[SPR], o3[SPR];
 #pragma unroll
       for (int u = 0; u < SPR; ++u) {
         const int i = min(i0 + u * nthr, H.ns - 1);
@@ -368,6 +438,9 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
         v[u][1] = srec[g + 1];
         v[u][2] = srec[g + 2];
         pn[u] = s_panel[gi];
+        cd[u] = s_code[gi];
+        o12[u] = e.y;
+        o3[u] = e.w;
       }
       double xv[SPR];
 #pragma unroll
@@ -376,25 +449,40 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
       for (int u = 0; u < SPR; ++u) {
         const int i = i0 + u * nthr;
         if (i >= H.ns) break;
-        // destination: own sources first (rank among them), the rest compacted after
-        int r = 0, hi = H.nspec;  // r = number of own sources at tile positions < i
-        while (r < hi) {
-          const int mid = (r + hi) >> 1;
-          if (spec[mid] < i) r = mid + 1;
-          else hi = mid;
+        const int sec = cd[u] & 3, pos = (cd[u] >> 2) & 3, rank = cd[u] >> 4;
+        int pt, rec;  // slots in the point planes (0, 1) and the record planes (2, 3)
+        if (sec == 0) {
+          // single point: own sources first (rank among them), the rest compacted after
+          const int sidx = (o12[u] & 0xffff) + rank;
+          int r = 0, hi = H.nspec;  // r = number of own sources at single positions < sidx
+          while (r < hi) {
+            const int mid = (r + hi) >> 1;
+            if (spec[mid] < sidx) r = mid + 1;
+            else hi = mid;
+          }
+          pt = rec = (r < H.nspec && spec[r] == sidx) ? r : H.nspec + sidx - r;
+        } else if (sec == 1) {
+          const int c = (o12[u] >> 16) + rank;
+          pt = H.n1 + 2 * c + pos;
+          rec = H.n1 + c;
+        } else {
+          const int c = o3[u] + rank;
+          pt = H.n1 + 2 * H.n2 + 3 * c + pos;
+          rec = H.n1 + H.n2 + c;
         }
-        const int dst = (r < H.nspec && spec[r] == i) ? r : H.nspec + i - r;
         const double sx = v[u][0].x - H.cx, sy = v[u][0].y - H.cy, sz = v[u][1].x - H.cz;
-        // dipole d = (w n) x[panel] (bemop.py:188-203, 213-216), times the -3/2 of the
-        // interaction body's r^-3 = -3/2 y^3 g
-        const double xs = -1.5 * xv[u];
-        const double dx = v[u][1].y * xs, dy = v[u][2].x * xs, dz = v[u][2].y * xs;
         const double ss = fma(sx, sx, fma(sy, sy, sz * sz));
-        const double ds = fma(dx, sx, fma(dy, sy, dz * sz));
-        sh2[dst] = make_double2(-2.0 * sx, -2.0 * sy);
-        sh2[max_src + dst] = make_double2(-2.0 * sz, ss);
-        sh2[2 * max_src + dst] = make_double2(dx, dy);
-        sh2[3 * max_src + dst] = make_double2(dz, -ds);
+        sh2[pt] = make_double2(-2.0 * sx, -2.0 * sy);
+        sh2[max_src + pt] = make_double2(-2.0 * sz, ss);
+        if (pos == 0) {
+          // dipole d = (w n) x[panel] (bemop.py:188-203, 213-216), times the -3/2 of the
+          // interaction body's r^-3 = -3/2 y^3 g; a cluster's first point writes the shared one
+          const double xs = -1.5 * xv[u];
+          const double dx = v[u][1].y * xs, dy = v[u][2].x * xs, dz = v[u][2].y * xs;
+          const double ds = fma(dx, sx, fma(dy, sy, dz * sz));
+          sh2[2 * max_src + rec] = make_double2(dx, dy);
+          sh2[3 * max_src + rec] = make_double2(dz, -ds);
+        }
       }
     }
     return true;
@@ -463,7 +551,8 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
     mbar_wait(&s_full[st], (unsigned)(k / NSTG) & 1u);
     if (threadIdx.x == 0) TR(k, 4);
     if (hdr[0] == 0) break;
-    const int ns = hdr[1], nt = hdr[2], out_off = hdr[3], nspec = hdr[4];
+    const int nt = hdr[2], out_off = hdr[3], nspec = hdr[4];
+    const int ns = hdr[5], n2 = hdr[6], n3 = hdr[7];  // (ns: the single points; then the clusters)
     // thread groups: nsl target slots (TPT targets each) x G source groups
     const int nsl = (nt + TPT - 1) / TPT;
     const int G = NCT / nsl;
@@ -514,6 +603,8 @@ k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4*
         if (j < ns) lapd_body<TPT, false>(u, j, tx, ty, tz, tt, self, acc);
 #endif
       }
+      lapd_run_clusters<TPT, 2>(sh2, max_src, ns, ns, n2, g, G, tx, ty, tz, tt, acc);
+      lapd_run_clusters<TPT, 3>(sh2, max_src, ns + n2, ns + 2 * n2, n3, g, G, tx, ty, tz, tt, acc);
     }
     if (threadIdx.x == 0) TR(k, 5);
     if (threadIdx.x == NCT - 32) TR(k, 6);
@@ -555,26 +646,71 @@ bool p2p_lapd_usable(const P2PAux* aux, int max_sources) {
 void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& items,
                    const std::vector<int>& p2p_src, const std::vector<int>& self_src_sorted,
                    cudaStream_t st) {
+  // tile sections per source leaf (see lapd_body_cl): the outer far-rule points of one panel
+  // inside one leaf form a cluster of 2 or 3; centroids (Gauss point 0, bemop.py:64-70) and lone
+  // outer points stay singles.  FMMBEM_P2P_CLUSTER=0 keeps every point single.
+  static const bool cluster = !(std::getenv("FMMBEM_P2P_CLUSTER") && std::atoi(std::getenv("FMMBEM_P2P_CLUSTER")) == 0);
+  const std::vector<int> perm = S.perm.download(st);
+  std::vector<int> cd(std::max<size_t>(perm.size(), 1), 0);
+  std::vector<int> c1(S.n_cells, 0), c2(S.n_cells, 0), c3(S.n_cells, 0);
+  {
+    std::vector<std::pair<int, int>> pts;  // (original index = 4 panel + k, sorted index)
+    for (const int leaf : S.h_leaves) {
+      const int s0 = S.h_body_start[leaf], cnt = S.h_body_count[leaf];
+      pts.clear();
+      for (int i = 0; i < cnt; ++i) pts.emplace_back(perm[s0 + i], s0 + i);
+      std::sort(pts.begin(), pts.end());
+      int r1 = 0, r2 = 0, r3 = 0;
+      for (size_t a = 0; a < pts.size();) {
+        size_t b = a;
+        while (b < pts.size() && pts[b].first / 4 == pts[a].first / 4) ++b;
+        size_t o = a;  // the panel's outer points [o, b)
+        if (pts[a].first % 4 == 0) cd[pts[o++].second] = 0 | (r1++ << 4);
+        const int m = (int)(b - o);
+        if (!cluster || m == 1) {
+          for (; o < b; ++o) cd[pts[o].second] = 0 | (r1++ << 4);
+        } else if (m == 2) {
+          for (int q = 0; q < 2; ++q) cd[pts[o + q].second] = 1 | (q << 2) | (r2 << 4);
+          ++r2;
+        } else if (m == 3) {
+          for (int q = 0; q < 3; ++q) cd[pts[o + q].second] = 2 | (q << 2) | (r3 << 4);
+          ++r3;
+        }
+        a = b;
+      }
+      c1[leaf] = r1;
+      c2[leaf] = r2;
+      c3[leaf] = r3;
+    }
+  }
   std::vector<int4> lt(std::max<size_t>(p2p_src.size(), 1), make_int4(0, 0, 0, 0));
   int64_t part_len = 0;
   for (const auto& it : items) part_len = std::max<int64_t>(part_len, it.out_off + T.h_body_count[it.tgt_leaf]);
   std::vector<int> sl(std::max<int64_t>(part_len, 1), -1), sp(std::max<int64_t>(part_len, 1), 0);
   std::vector<int> nspec_of(items.size(), 0);
+  std::vector<int4> sect(items.size(), make_int4(0, 0, 0, 0));  // (n1, n2, n3, ns) per item
   max_leaves = 1;
   max_tgt = 1;
   for (const auto& it : items) {
-    int off = 0;
+    int off = 0, o1 = 0, o2 = 0, o3 = 0;
     for (int k = it.pair_begin; k < it.pair_end; ++k) {
       const int leaf = p2p_src[k];
-      lt[k] = make_int4(S.h_body_start[leaf], S.h_body_count[leaf], off, 0);
+      FMM_REQUIRE(o1 < 65536 && o2 < 32768, "P2P: item too large for the packed section offsets");
+      lt[k] = make_int4(S.h_body_start[leaf], o1 | (o2 << 16), off, o3);
       off += S.h_body_count[leaf];
+      o1 += c1[leaf];
+      o2 += c2[leaf];
+      o3 += c3[leaf];
     }
+    sect[&it - items.data()] = make_int4(o1, o2, o3, off);
     const int t0 = T.h_body_start[it.tgt_leaf], nt = T.h_body_count[it.tgt_leaf];
-    std::vector<std::pair<int, int>> own;  // (tile position, target)
+    std::vector<std::pair<int, int>> own;  // (position among the item's singles, target)
     for (int l = 0; l < nt; ++l) {
       const int gs = self_src_sorted[t0 + l];
-      for (int k = it.pair_begin; k < it.pair_end; ++k)
-        if (gs >= lt[k].x && gs < lt[k].x + lt[k].y) own.emplace_back(lt[k].z + gs - lt[k].x, l);
+      for (int k = it.pair_begin; k < it.pair_end; ++k) {
+        const int leaf = p2p_src[k];
+        if (gs >= lt[k].x && gs < lt[k].x + S.h_body_count[leaf]) own.emplace_back((lt[k].y & 0xffff) + (cd[gs] >> 4), l);
+      }
     }
     std::sort(own.begin(), own.end());
     for (size_t r = 0; r < own.size(); ++r) {
@@ -590,10 +726,12 @@ void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& ite
   for (size_t r = 0; r < ord.size(); ++r) {
     const P2PItem& it = items[ord[r]];
     LapdHdr& e = h[r];
-    e.item = ord[r];
     e.pair_begin = it.pair_begin;
     e.nl = it.pair_end - it.pair_begin;
-    e.ns = it.pair_end > it.pair_begin ? lt[it.pair_end - 1].z + lt[it.pair_end - 1].y : 0;
+    e.ns = sect[ord[r]].w;
+    e.n1 = sect[ord[r]].x;
+    e.n2 = sect[ord[r]].y;
+    e.n3 = sect[ord[r]].z;
     e.t0 = T.h_body_start[it.tgt_leaf];
     e.nt = T.h_body_count[it.tgt_leaf];
     e.out_off = it.out_off;
@@ -603,11 +741,21 @@ void P2PAux::build(const Tree& S, const Tree& T, const std::vector<P2PItem>& ite
     e.cz = T.h_cz[it.tgt_leaf];
   }
   n_items = (int)items.size();
+  if (std::getenv("FMMBEM_P2P_STATS")) {
+    double w1 = 0, w2 = 0, w3 = 0, wspec = 0;
+    for (size_t i = 0; i < items.size(); ++i) {
+      const double nt = T.h_body_count[items[i].tgt_leaf];
+      w1 += nt * sect[i].x, w2 += nt * 2.0 * sect[i].y, w3 += nt * 3.0 * sect[i].z, wspec += nt * nspec_of[i];
+    }
+    std::fprintf(stderr, "[fmmbem] P2P tile sections by interactions: singles %.4f (own %.4f) pairs %.4f triples %.4f of %.4g\n",
+                 w1 / (w1 + w2 + w3), wspec / (w1 + w2 + w3), w2 / (w1 + w2 + w3), w3 / (w1 + w2 + w3), w1 + w2 + w3);
+  }
   p2p_trace_buffer();  // (allocated here, outside any stream capture)
   hdr.upload(h, st);
   ltab.upload(lt, st);
   slot.upload(sl, st);
   spec.upload(sp, st);
+  code.upload(cd, st);
   ready = true;
 }
 
@@ -651,7 +799,7 @@ void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const dou
   if (grid > 0)
     kern<<<grid, nthr, smem, st>>>(T, aux.hdr.get(), aux.n_items, aux.ltab.get(), aux.slot.get(),
                                    aux.spec.get(), max_src,
-                                   aux.max_leaves, aux.max_tgt, srec, s_panel, x, part, sched,
+                                   aux.max_leaves, aux.max_tgt, srec, s_panel, aux.code.get(), x, part, sched,
                                    p2p_trace_buffer());
   FMM_LAUNCH_CHECK();
 }
