@@ -10,7 +10,7 @@ import sys
 
 import numpy as np
 
-os.environ["FMMBEM_P2P_TRACE"] = "1"
+os.environ.setdefault("FMMBEM_P2P_TRACE", "1")  # = stride: every stride-th item of a CTA is traced (32 slots)
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 from paper_1506_05957_b200 import _native  # noqa: E402
 from paper_1506_05957_b200.configs import CONFIGS  # noqa: E402
@@ -56,3 +56,14 @@ print("ns: cta start spread", int(starts.max() - t0), "first item staged (median
       "cta end min/median/max", int(ends.min() - t0), int(np.median(ends - t0)), int(ends.max() - t0))
 last = sorted(((c, [int(t[c, k, 2] - t[c, k, 1]) for k in range(32) if t[c, k, 2]]) for c in ctas[:1]))
 print("producer stage cycles per item (cta 0):", last)
+
+# per traced item (mean over CTAs): producer wait / stage, consumer wait FULL / busy, ns
+rows = []
+for k in range(32):
+    v = [(t[c, k, 1] - t[c, k, 0], t[c, k, 2] - t[c, k, 1], t[c, k, 4] - t[c, k, 3], t[c, k, 7] - t[c, k, 4])
+         for c in ctas if t[c, k, 2] != 0 and t[c, k, 7] != 0 and t[c, k, 0] != 0]
+    if v:
+        rows.append((k, len(v)) + tuple(int(np.mean([r[j] for r in v])) for j in range(4)))
+print("slot ctas p_wait p_stage c_waitfull c_busy (ns)")
+for r in rows:
+    print(*r)
