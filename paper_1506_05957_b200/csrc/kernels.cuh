@@ -35,7 +35,8 @@ void launch_m2m(const Tree& S, const std::vector<int>& level_off, const int* cel
 void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
                 cudaStream_t st, const int4* gitems = nullptr, int n_gitems = -1,
                 const int* cells = nullptr, int n_cells = -1, const int* gpair = nullptr,
-                const int4* citems = nullptr, int n_citems = -1, const int* cpair = nullptr);
+                const int4* citems = nullptr, int n_citems = -1, const int* cpair = nullptr,
+                const RotGroups* rg = nullptr);
 void compute_igrid_full(const double* d_off, int n_off, int order, double2* out, cudaStream_t s);
 void compute_rot_tables(const double* d_off, int n_off, int P, double* out, double* geo,
                         cudaStream_t s);
@@ -44,8 +45,13 @@ size_t rot_frag_size(int P);
 inline size_t rot_aux_size(int P) { return (size_t)(4 * P + 4); }
 void build_rot_aux(const double* geo, int n_off, int P, double* aux, cudaStream_t s);
 void build_rot_frag(const double* rot, int n_off, int P, double* out, cudaStream_t s);
+// rg (RotGroups over class-grouped items) and FMMBEM_M2L_SHARED=1: the shared-table kernel, one
+// CTA per group with the direction's tables staged in shared memory by bulk async copies (TMA)
+// and the multipoles prefetched by cp.async; otherwise the per-warp kernel that reads the tables
+// from L2 (the default: measured 1-2 % faster, both are bound by shared/L1 operand bandwidth)
 void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
-                    int C, const double2* M, double2* pout, cudaStream_t st, bool cls);
+                    int C, const double2* M, double2* pout, cudaStream_t st, bool cls,
+                    const RotGroups* rg = nullptr);
 constexpr int M2L_ROT_MIN_P = 3;  // rotation-based M2L from this order up
 void launch_m2l_gather(const Plan& plan, int p, int C, const double2* part, double2* L, cudaStream_t st);
 // M2M by rotation (point and shoot, DMMA): per-child contributions into cout, then the

@@ -193,73 +193,68 @@ __global__ void k_rot_aux(const double* __restrict__ geo, int n_off, int P, doub
 // CLS: the item's vectors may come from different offsets of one class (same polar-angle
 // tables and |D|): the azimuthal phases are read per vector into registers; otherwise the
 // item shares one offset and its phases are read once into shared memory.
-template <int P, bool CLS>
-__global__ void __launch_bounds__(ROT_WARPS * 32)
-k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ gpair,
-          const int* __restrict__ pair_src, const int* __restrict__ pair_off, const double* __restrict__ frag,
-          const int* __restrict__ dir, int ttot,
-          const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
-          double2* __restrict__ pout) {
+// One warp unit of the rotation M2L: the three stages for 8 vectors whose offsets share the
+// polar-angle tables `tabs` (4 tables, tstride doubles apart) and |D|.  The caller has filled
+// the unit's buffers wsh: zz (and ph when !CLS); inputs per lane:
+//   !SH: msrc = the multipole of vector fr = lane >> 2 (null: none), read from global memory
+//        degree by degree;  SH: the 8 multipoles are already staged in bre / bim ([H][8] planes)
+//        and the tables are in shared memory
+//   paA  = (CLS) the phases e^{-ik phi} of vector fr's offset
+//   dst0/dst1, po0/po1 = the result slots and phases of vectors 2 fc and 2 fc + 1 (fc = lane & 3)
+//   after(j) runs once stage C has read degree j's rows of the planes (they are free from then on)
+template <int P, bool CLS, bool SH, class After>
+__device__ __forceinline__ void
+m2l_rot_core(double* __restrict__ wsh, const int lane, const double* __restrict__ tabs, const size_t tstride,
+             const double2* __restrict__ msrc, const double2* __restrict__ paA, double2* __restrict__ dst0,
+             double2* __restrict__ dst1, const double2* __restrict__ po0, const double2* __restrict__ po1,
+             After&& after) {
   constexpr int H = hcount(P);
-  constexpr int WS = 16 * H + 4 * P + 4;
-  extern __shared__ double sh[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int unit = blockIdx.x * ROT_WARPS + warp;
-  const int item = unit / C, oct = unit % C;
-  if (item >= n_items) return;
-  const int4 it = items[item];
-  const int nvec = (it.z - it.y) * C, v0 = oct * 8;
-  if (v0 >= nvec) return;
-  double* bre = sh + (size_t)warp * WS;                    // [H][8] real parts
+  double* bre = wsh;                                       // [H][8] real parts
   double* bim = bre + 8 * H;                               // [H][8] imaginary parts
   double2* ph = reinterpret_cast<double2*>(bim + 8 * H);   // [P+1] e^{-ik phi}
   double* zz = reinterpret_cast<double*>(ph + P + 1);      // [2P+1] N! / r^(N+1)
-  const int u = it.x;
-  {
-    const double* A = aux + (size_t)u * aux_stride(aux_p);
-    double* sp = reinterpret_cast<double*>(ph);
-#pragma unroll
-    for (int i = lane; i < 2 * (P + 1); i += 32) sp[i] = A[i];
-#pragma unroll
-    for (int i = lane; i <= 2 * P; i += 32) zz[i] = A[2 * (aux_p + 1) + i];
-  }
   const int fr = lane >> 2, fc = lane & 3;  // fragment row / column-in-k
-  const double* T = frag + (size_t)dir[u] * 4 * ttot * 32 + lane;
+  const double* T = tabs + lane;
   auto load = [&](Frag& f, int tab, int n) {
     const int mt = frag_mt(n), ks = frag_ks(n);
-    const double* tr = T + (size_t)(tab * ttot + frag_base(n)) * 32;
-    const double* ti = tr + (size_t)ttot * 32;
+    const double* tr = T + (SH ? 0 : tab) * tstride + (size_t)frag_base(n) * 32;
+    const double* ti = tr + tstride;
 #pragma unroll
     for (int q = 0; q < 3; ++q)
 #pragma unroll
       for (int t = 0; t < FRAG_KS_MAX; ++t)
         if (q < mt && t < ks) {
-          f.r[q][t] = __ldg(tr + (q * ks + t) * 32);
-          f.i[q][t] = __ldg(ti + (q * ks + t) * 32);
+          if constexpr (SH) {
+            if (tab == 0) {
+              f.r[q][t] = tr[(q * ks + t) * 32];
+              f.i[q][t] = ti[(q * ks + t) * 32];
+            } else {
+              // stage C's operators are the transposes of stage A's (SC[k][l] = SA[l][k], from
+              // d_{-l,k} = (-1)^(l+k) d_{l,-k}): element (8q + fr, 4t + fc) of the transpose is
+              // lane (4 (t & 1) + fc, fr & 3) of SA's tile (row tile t / 2, k-step 2q + fr / 4) --
+              // two tiles at the same bank offsets, conflict-free.  Rows past the degree (k-step
+              // clamped) only feed result rows that are dropped.
+              const int kk = min(2 * q + (lane >> 4), ks - 1);
+              const int o = ((t >> 1) * ks + kk) * 32 + (4 * (t & 1) + (lane & 3)) * 4 + ((lane >> 2) & 3) - lane;
+              f.r[q][t] = tr[o];
+              f.i[q][t] = ti[o];
+            }
+          } else {
+            f.r[q][t] = __ldg(tr + (q * ks + t) * 32);
+            f.i[q][t] = __ldg(ti + (q * ks + t) * 32);
+          }
         }
   };
   // stage A: Re/Im M'_n^m = SA_re/im[m][k] Re/Im (e^{-ik phi} M_n^k); the B operand
-  // (k = 4t + fc, vector fr) comes straight from global memory, so the degrees are
-  // independent and need no synchronisation; next degree's operands are in flight
-  const double2* msrc = nullptr;
+  // (k = 4t + fc, vector fr) comes straight from global memory (or the staged planes), so the
+  // degrees are independent and need no synchronisation; next degree's operands are in flight
   // azimuthal phases e^{-ik phi} of each vector's own offset (the item's pairs share the
   // polar-angle tables and |D|, not necessarily phi): stage A's column fr, outputs 2fc, 2fc+1
-  const int astr = aux_stride(aux_p);
   double2 phA[CLS ? FRAG_KS_MAX : 1];  // (CLS) e^{-ik phi} of column fr's offset at k = 4t + fc
-  {
-    const int vg = v0 + fr;
-    int uo = u;
-    if (vg < nvec) {
-      const int pr = gpair[it.y + vg / C];
-      msrc = M + ((size_t)pair_src[pr] * C + vg % C) * H;
-      uo = pair_off[pr];
-    }
-    if constexpr (CLS) {
-      const double2* pa = reinterpret_cast<const double2*>(aux + (size_t)uo * astr);
+  if constexpr (CLS) {
 #pragma unroll
-      for (int t = 0; t < FRAG_KS_MAX; ++t)
-        phA[t] = 4 * t + fc <= P ? __ldg(pa + 4 * t + fc) : make_double2(0.0, 0.0);
-    }
+    for (int t = 0; t < FRAG_KS_MAX; ++t)
+      phA[t] = 4 * t + fc <= P ? __ldg(paA + 4 * t + fc) : make_double2(0.0, 0.0);
   }
   __syncwarp();  // ph, zz
   struct BIn {
@@ -271,7 +266,10 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
     for (int t = 0; t < FRAG_KS_MAX; ++t)
       if (t < ks) {
         const int col = t * 4 + fc;
-        b.m[t] = (msrc && col <= n) ? __ldg(msrc + hb + col) : make_double2(0.0, 0.0);
+        if constexpr (SH)
+          b.m[t] = col <= n ? make_double2(bre[(hb + col) * 8 + fr], bim[(hb + col) * 8 + fr]) : make_double2(0.0, 0.0);
+        else
+          b.m[t] = (msrc && col <= n) ? __ldg(msrc + hb + col) : make_double2(0.0, 0.0);
       }
   };
   double2 ar[3], ai[3];
@@ -366,6 +364,9 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
         const int j = k + q * 8 + fr;
         if (q < jt && j <= P) {
           const int hj = j * (j + 1) / 2 + k;
+          // (SH: stage C runs on the transposed stage-A tables, whose column l = 0 is twice
+          // SC's: SC_re[k][0] = a_{0,k} = SA_re[0][k] / 2 -- folded in here)
+          if (SH && k == 0) br_[w][q] = make_double2(0.5 * br_[w][q].x, 0.5 * br_[w][q].y);
           *reinterpret_cast<double2*>(bre + hj * 8 + 2 * fc) = br_[w][q];
           *reinterpret_cast<double2*>(bim + hj * 8 + 2 * fc) = bi_[w][q];
         }
@@ -392,18 +393,14 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
           }
       }
   };
-  // stage C and the output phase; lane owns vectors v0 + 2 fc and v0 + 2 fc + 1
-  double2* dst[2];
+  // stage C and the output phase; lane owns vectors 2 fc and 2 fc + 1
+  double2* dst[2] = {dst0, dst1};
   double2 phO[2][CLS ? 3 : 1];  // (CLS) e^{-ik phi} of output vector 2 fc + w at k = 8 q + fr
+  if constexpr (CLS) {
 #pragma unroll
-  for (int w = 0; w < 2; ++w) {
-    const int vg = v0 + 2 * fc + w;
-    const int pr = vg < nvec ? gpair[it.y + vg / C] : 0;
-    dst[w] = vg < nvec ? pout + ((size_t)pr * C + vg % C) * H : nullptr;
-    if constexpr (CLS) {
-      const double2* po = reinterpret_cast<const double2*>(aux + (size_t)(vg < nvec ? pair_off[pr] : u) * astr);
-#pragma unroll
-      for (int q = 0; q < 3; ++q) phO[w][q] = 8 * q + fr <= P ? __ldg(po + 8 * q + fr) : make_double2(0.0, 0.0);
+    for (int q = 0; q < 3; ++q) {
+      phO[0][q] = 8 * q + fr <= P ? __ldg(po0 + 8 * q + fr) : make_double2(0.0, 0.0);
+      phO[1][q] = 8 * q + fr <= P ? __ldg(po1 + 8 * q + fr) : make_double2(0.0, 0.0);
     }
   }
 #pragma unroll
@@ -411,24 +408,266 @@ k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ g
     Frag nxt;
     if (j < P) load(nxt, 2, j + 1);
     mult(cur, j);
+    after(j);
     const int hb = j * (j + 1) / 2;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       const int k = q * 8 + fr;
       if (q < frag_mt(j) && k <= j) {
         const double2 e0 = CLS ? phO[0][CLS ? q : 0] : ph[k], e1 = CLS ? phO[1][CLS ? q : 0] : ph[k];
-        if (dst[0]) dst[0][hb + k] = cmul(e0, make_double2(ar[q].x, ai[q].x));
-        if (dst[1]) dst[1][hb + k] = cmul(e1, make_double2(ar[q].y, ai[q].y));
+        double2 o0 = make_double2(ar[q].x, ai[q].x), o1 = make_double2(ar[q].y, ai[q].y);
+        if (SH && k == 0) {
+          // transposed tables: SC_re[0][l] = 2 SA_re[l][0] (l > 0; the l = 0 half is folded into
+          // stage B), SC_im[0][l] = 0 (the order-0 coefficients of a real field are real)
+          o0 = make_double2(2.0 * o0.x, 0.0);
+          o1 = make_double2(2.0 * o1.x, 0.0);
+        }
+        if (dst[0]) dst[0][hb + k] = cmul(e0, o0);
+        if (dst[1]) dst[1][hb + k] = cmul(e1, o1);
       }
     }
     if (j < P) cur = nxt;
   }
 }
 
+// v1: one warp unit per warp, two units per CTA, the tables read from L2 by every warp
+// (also the offset-grouped mode, CLS = false: one offset and one phase table per item)
+template <int P, bool CLS>
+__global__ void __launch_bounds__(ROT_WARPS * 32)
+k_m2l_rot(const int4* __restrict__ items, int n_items, const int* __restrict__ gpair,
+          const int* __restrict__ pair_src, const int* __restrict__ pair_off, const double* __restrict__ frag,
+          const int* __restrict__ dir, int ttot,
+          const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
+          double2* __restrict__ pout) {
+  constexpr int H = hcount(P);
+  constexpr int WS = 16 * H + 4 * P + 4;
+  extern __shared__ double sh[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * ROT_WARPS + warp;
+  const int item = unit / C, oct = unit % C;
+  if (item >= n_items) return;
+  const int4 it = items[item];
+  const int nvec = (it.z - it.y) * C, v0 = oct * 8;
+  if (v0 >= nvec) return;
+  double* wsh = sh + (size_t)warp * WS;
+  double* sp = wsh + 16 * H;      // [P+1] e^{-ik phi} as (re, im)
+  double* zz = sp + 2 * (P + 1);  // [2P+1] N! / r^(N+1)
+  const int u = it.x, astr = aux_stride(aux_p);
+  {
+    const double* A = aux + (size_t)u * astr;
+#pragma unroll
+    for (int i = lane; i < 2 * (P + 1); i += 32) sp[i] = A[i];
+#pragma unroll
+    for (int i = lane; i <= 2 * P; i += 32) zz[i] = A[2 * (aux_p + 1) + i];
+  }
+  const int fr = lane >> 2, fc = lane & 3;
+  const double2* msrc = nullptr;
+  int uo = u;
+  {
+    const int vg = v0 + fr;
+    if (vg < nvec) {
+      const int pr = gpair[it.y + vg / C];
+      msrc = M + ((size_t)pair_src[pr] * C + vg % C) * H;
+      uo = pair_off[pr];
+    }
+  }
+  double2* dst[2];
+  const double2* po[2];
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const int vg = v0 + 2 * fc + w;
+    const int pr = vg < nvec ? gpair[it.y + vg / C] : 0;
+    dst[w] = vg < nvec ? pout + ((size_t)pr * C + vg % C) * H : nullptr;
+    po[w] = reinterpret_cast<const double2*>(aux + (size_t)((CLS && vg < nvec) ? pair_off[pr] : u) * astr);
+  }
+  m2l_rot_core<P, CLS, false>(wsh, lane, frag + (size_t)dir[u] * 4 * ttot * 32, (size_t)ttot * 32, msrc,
+                              reinterpret_cast<const double2*>(aux + (size_t)uo * astr), dst[0], dst[1], po[0],
+                              po[1], [](int) {});
+}
+
+// ---- v2: the direction's tables staged once per CTA by bulk async copies (TMA) --------------
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "MBW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MBW_%=;\n"
+      "}\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (16-byte aligned, a multiple of 16 bytes), completion on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+
+constexpr int ROT2_GROUP = 24;  // items per CTA group (divisible by every ROT2 warp count)
+__host__ __device__ constexpr size_t rot2_tab_doubles(int P) { return (size_t)2 * frag_base(P + 1) * 32; }
+__host__ __device__ constexpr size_t rot2_ws_doubles(int P) { return (size_t)16 * hcount(P) + 4 * P + 4; }
+__host__ __device__ constexpr size_t rot2_smem(int P, int W) {
+  return (rot2_tab_doubles(P) + (size_t)W * rot2_ws_doubles(P)) * sizeof(double) + 16;
+}
+// warps per CTA: the most of {12, 8, 6, 4, 3, 2, 1} whose buffers fit beside the tables; low
+// orders take 8 (several CTAs per SM)
+__host__ __device__ constexpr int rot2_warps(int P) {
+  constexpr int cand[7] = {12, 8, 6, 4, 3, 2, 1};
+  if (P <= 10) return 8;
+  for (int i = 0; i < 7; ++i)
+    if (rot2_smem(P, cand[i]) <= (size_t)227 * 1024) return cand[i];
+  return 1;
+}
+
+// group = (direction table, first item, end item) of class-grouped items whose offsets share one
+// polar angle; the CTA's warps take the items' warp units (item x channel octet) round robin.
+// vecs[8 item + a] = (pair slot, source cell, offset id, 0) of the item's a-th pair (slot -1:
+// none): one independent load per unit (fetched one unit ahead), then all the unit's multipoles
+// are read in one burst into the stage planes -- no dependent global loads inside the stages.
+template <int P, int W>
+__global__ void __launch_bounds__(W * 32)
+k_m2l_rot2(const int4* __restrict__ groups, const int4* __restrict__ vecs, const double* __restrict__ frag,
+           int ttot, const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
+           double2* __restrict__ pout) {
+  constexpr int H = hcount(P);
+  constexpr int NT = frag_base(P + 1);  // tiles per table up to degree P
+  constexpr size_t WS = rot2_ws_doubles(P);
+  extern __shared__ __align__(128) double sh[];
+  double* tabs = sh;                                 // [2][NT * 32]: SA_re, SA_im (stage C reads them transposed)
+  double* wbuf = sh + rot2_tab_doubles(P);           // [W][WS]
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(wbuf + (size_t)W * WS);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 g = groups[blockIdx.x];
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar, 2u * NT * 32u * (unsigned)sizeof(double));
+    const double* src = frag + (size_t)g.x * 4 * ttot * 32;
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+      bulk_g2s(tabs + (size_t)t * NT * 32, src + (size_t)t * ttot * 32, NT * 32u * (unsigned)sizeof(double), bar);
+  }
+  __syncthreads();  // the barrier is initialised before anyone polls it
+  double* wsh = wbuf + (size_t)warp * WS;
+  double* bre = wsh;
+  double* bim = wsh + 8 * H;
+  double* zz = wsh + 16 * H + 2 * (P + 1);
+  const int astr = aux_stride(aux_p);
+  const int va = lane & 7, fr = lane >> 2, fc = lane & 3;
+  // lane's vector in the load role: va of the unit's octet
+  auto fetch = [&](int unit) -> int4 {  // x = -2: no such unit
+    if (unit >= g.z * C) return make_int4(-2, 0, 0, 0);
+    const int vg = (unit % C) * 8 + va;  // vector of the item = (pair vg / C, channel vg % C)
+    int4 e = __ldg(vecs + (size_t)(unit / C) * 8 + vg / C);
+    e.w = vg % C;
+    return e;
+  };
+  // degree j of a unit's 8 multipoles into the planes, asynchronously: lane's vector va,
+  // coefficients i = hb + (lane >> 3) + 4 r; a missing vector's rows are zero-filled.  Each
+  // 16-byte coefficient goes as two 8-byte copies (the planes split real and imaginary parts).
+  auto prefetch = [&](const int4& rec, int j) {
+    if (rec.x == -2) return;  // no such unit
+    const double2* mv = M + ((size_t)rec.y * C + rec.w) * H;
+    const unsigned sz = rec.x >= 0 ? 8u : 0u;
+    const int hb = j * (j + 1) / 2;
+    for (int i = hb + (lane >> 3); i <= hb + j; i += 4) {
+      const double* s = reinterpret_cast<const double*>(mv + i);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(bre + i * 8 + va)),
+                   "l"(s), "r"(sz)
+                   : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(bim + i * 8 + va)),
+                   "l"(s + 1), "r"(sz)
+                   : "memory");
+    }
+  };
+  int unit = g.y * C + warp;
+  int4 cur = fetch(unit);
+  if (cur.x != -2) {
+#pragma unroll
+    for (int j = 0; j <= P; ++j) prefetch(cur, j);
+  }
+  bool first = true;
+  for (; unit < g.z * C; unit += W) {
+    int4 nxt = fetch(unit + W);
+    if (__shfl_sync(0xffffffffu, nxt.x, 0) == -1) nxt.x = -2;  // an octet past the item's vectors: skipped
+    if (__shfl_sync(0xffffffffu, cur.x, 0) < 0) {  // a skipped octet: burst-load the one after it
+      cur = nxt;
+      if (cur.x != -2) {
+#pragma unroll
+        for (int j = 0; j <= P; ++j) prefetch(cur, j);
+      }
+      continue;
+    }
+    // the unit's |D| factors, from any member offset (the octet's first vector exists)
+    const int u0 = __shfl_sync(0xffffffffu, cur.z, 0);
+    {
+      const double* A = aux + (size_t)u0 * astr + 2 * (aux_p + 1);
+#pragma unroll
+      for (int i = lane; i <= 2 * P; i += 32) zz[i] = A[i];
+    }
+    // roles of the stages: column fr (stage A), outputs 2 fc and 2 fc + 1 (stage C)
+    const int offA = __shfl_sync(0xffffffffu, cur.z, fr);
+    int prO[2], offO[2], chO[2];
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      prO[w] = __shfl_sync(0xffffffffu, cur.x, 2 * fc + w);
+      offO[w] = __shfl_sync(0xffffffffu, cur.z, 2 * fc + w);
+      chO[w] = __shfl_sync(0xffffffffu, cur.w, 2 * fc + w);
+    }
+    double2* d0 = prO[0] >= 0 ? pout + ((size_t)prO[0] * C + chO[0]) * H : nullptr;
+    double2* d1 = prO[1] >= 0 ? pout + ((size_t)prO[1] * C + chO[1]) * H : nullptr;
+    if (first) {
+      mbar_wait(bar, 0);  // the tables have landed
+      first = false;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this unit's multipoles are in the planes
+    __syncwarp();
+    // the next unit's multipoles follow stage C through the planes, degree by degree
+    m2l_rot_core<P, true, true>(wsh, lane, tabs, (size_t)NT * 32, nullptr,
+                                reinterpret_cast<const double2*>(aux + (size_t)offA * astr), d0, d1,
+                                reinterpret_cast<const double2*>(aux + (size_t)offO[0] * astr),
+                                reinterpret_cast<const double2*>(aux + (size_t)offO[1] * astr),
+                                [&](int j) { prefetch(nxt, j); });
+    cur = nxt;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 template <int P>
 void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int C,
-                  const double2* M, double2* pout, cudaStream_t st, bool cls) {
+                  const double2* M, double2* pout, cudaStream_t st, bool cls, const int4* groups, int n_groups,
+                  const int4* vecs) {
   constexpr int H = hcount(P);
+  // the shared-table kernel is opt-in (FMMBEM_M2L_SHARED=1): both kernels run at the same
+  // shared-memory / L1 operand bandwidth (one 256-byte fragment per DMMA), and the per-warp
+  // kernel measured 1-2 % faster end to end (cfg5 460.9 vs 456.0, cfg2 5 858 vs 5 728 mat-vecs/s)
+  const char* sel = std::getenv("FMMBEM_M2L_SHARED");
+  if (cls && groups && vecs && n_groups > 0 && sel && sel[0] == '1') {
+    constexpr int W = rot2_warps(P);
+    constexpr size_t smem2 = rot2_smem(P, W);
+    static DeviceOnce attr2;
+    if (attr2.first()) {
+      FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot2<P, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      attr2.mark();
+    }
+    k_m2l_rot2<P, W><<<(unsigned)n_groups, W * 32, smem2, st>>>(
+        groups, vecs, plan.rotf.get(), frag_base(plan.rot_p + 1), plan.rot_aux.get(), plan.rot_p, M, C, pout);
+    FMM_LAUNCH_CHECK();
+    return;
+  }
   const size_t smem = (size_t)ROT_WARPS * (16 * H + 4 * P + 4) * sizeof(double);
   static DeviceOnce attr;
   if (attr.first()) {
@@ -448,10 +687,13 @@ void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_
 template <int... Ps>
 void launch_rot_dispatch(std::integer_sequence<int, Ps...>, int p, const Plan& plan,
                          const int4* gitems, const int* gpair, int n_items, int C,
-                         const double2* M, double2* pout, cudaStream_t st, bool cls) {
+                         const double2* M, double2* pout, cudaStream_t st, bool cls, const int4* groups,
+                         int n_groups, const int4* vecs) {
   bool done = false;
   ((p == Ps + M2L_ROT_MIN_P && !done
-        ? (launch_rot_p<Ps + M2L_ROT_MIN_P>(plan, gitems, gpair, n_items, C, M, pout, st, cls), done = true)
+        ? (launch_rot_p<Ps + M2L_ROT_MIN_P>(plan, gitems, gpair, n_items, C, M, pout, st, cls, groups, n_groups,
+                                            vecs),
+           done = true)
         : false),
    ...);
   FMM_REQUIRE(done, "rotation M2L order out of range");
@@ -789,11 +1031,39 @@ void build_rot_aux(const double* geo, int n_off, int P, double* aux, cudaStream_
 }
 
 void launch_m2l_rot(const Plan& plan, const int4* gitems, const int* gpair, int n_items, int p,
-                    int C, const double2* M, double2* pout, cudaStream_t st, bool cls) {
+                    int C, const double2* M, double2* pout, cudaStream_t st, bool cls, const RotGroups* rg) {
   if (n_items <= 0) return;
   FMM_REQUIRE(p <= plan.rot_p, "rotation tables not prepared for this order");
   launch_rot_dispatch(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, plan, gitems,
-                      gpair, n_items, C, M, pout, st, cls);
+                      gpair, n_items, C, M, pout, st, cls, rg ? rg->groups.get() : nullptr, rg ? rg->n_groups : 0,
+                      rg ? rg->vecs.get() : nullptr);
+}
+
+// CTA groups of the shared-table rotation M2L: consecutive class-grouped items of one direction
+// table, <= ROT2_GROUP items each, cut evenly; and the items' pairs as (slot, source cell,
+// offset id, 0) records, 8 per item
+void RotGroups::build(const std::vector<int4>& items, const std::vector<int>& cpair, const std::vector<int>& pair_src,
+                      const std::vector<int>& pair_off, const std::vector<int>& dir_of_off, cudaStream_t s) {
+  std::vector<int4> g, v(std::max<size_t>(items.size(), 1) * 8, make_int4(-1, 0, 0, 0));
+  for (size_t i = 0; i < items.size();) {
+    size_t j = i;
+    const int d = dir_of_off[items[i].x];
+    while (j < items.size() && dir_of_off[items[j].x] == d) ++j;
+    const int64_t u0 = (int64_t)i, len = (int64_t)(j - i), nch = (len + ROT2_GROUP - 1) / ROT2_GROUP;
+    for (int64_t q = 0; q < nch; ++q)
+      g.push_back(make_int4(d, (int)(u0 + len * q / nch), (int)(u0 + len * (q + 1) / nch), 0));
+    i = j;
+  }
+  for (size_t i = 0; i < items.size(); ++i) {
+    FMM_REQUIRE(items[i].z - items[i].y <= 8 && items[i].z > items[i].y, "rotation M2L item size");
+    for (int k = items[i].y; k < items[i].z; ++k) {
+      const int pr = cpair[k];
+      v[i * 8 + (k - items[i].y)] = make_int4(pr, pair_src[pr], pair_off[pr], 0);
+    }
+  }
+  n_groups = (int)g.size();
+  groups.upload(g.empty() ? std::vector<int4>(1) : g, s);
+  vecs.upload(v, s);
 }
 
 namespace {

@@ -750,7 +750,7 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     FMM_CUDA(cudaEventRecord(op.ev_basis, s));
     FMM_CUDA(cudaStreamWaitEvent(op.s_far2, op.ev_basis, 0));
     launch_m2l_rot(pl, pl.d_m2l_ci_leaf.get(), pl.m2l_cp_leaf.get(), (int)pl.m2l_ci_leaf.size(), c.p, C,
-                   op.M.get(), op.m2l_part.get(), op.s_far2, true);
+                   op.M.get(), op.m2l_part.get(), op.s_far2, true, &pl.m2l_rg_leaf);
     FMM_CUDA(cudaEventRecord(op.ev_m2l2, op.s_far2));
     leaf_m2l_forked = true;
   };
@@ -789,17 +789,17 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
     record(op, ST_M2L, false, s);
     if (split_m2l) {
       launch_m2l_rot(pl, pl.d_m2l_ci_rest.get(), pl.m2l_cp_rest.get(), (int)pl.m2l_ci_rest.size(), c.p, C,
-                     op.M.get(), op.m2l_part.get(), s, true);
+                     op.M.get(), op.m2l_part.get(), s, true, &pl.m2l_rg_rest);
       if (leaf_m2l_forked)
         FMM_CUDA(cudaStreamWaitEvent(s, op.ev_m2l2, 0));
       else  // (the upward path did not fork it)
         launch_m2l_rot(pl, pl.d_m2l_ci_leaf.get(), pl.m2l_cp_leaf.get(), (int)pl.m2l_ci_leaf.size(), c.p, C,
-                       op.M.get(), op.m2l_part.get(), s, true);
+                       op.M.get(), op.m2l_part.get(), s, true, &pl.m2l_rg_leaf);
       launch_m2l_gather(pl, c.p, C, op.m2l_part.get(), op.L.get(), s);
     } else if (sharded)
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s, sw.gitems.get(),
                  (int)sw.gitems_h.size(), sw.gather_cells.get(), sw.n_gather_cells, sw.gpair.get(),
-                 sw.citems.get(), sw.n_citems, sw.cpair.get());
+                 sw.citems.get(), sw.n_citems, sw.cpair.get(), &sw.rg);
     else
       launch_m2l(pl, c.p, C, op.M.get(), op.L.get(), op.m2l_part.get(), s);
     record(op, ST_M2L, true, s);

@@ -60,6 +60,7 @@ struct ShardWork {
   DevBuf<int4> citems;  // class-grouped (rotation M2L) items restricted to the shard
   DevBuf<int> cpair;
   int n_citems = 0;
+  RotGroups rg;  // their CTA groups and pair records (shared-table rotation M2L)
   DevBuf<int> gather_cells;
   int n_gather_cells = 0;
   std::vector<int> l2l_off;

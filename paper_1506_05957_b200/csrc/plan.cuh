@@ -56,6 +56,16 @@ struct P2PItem {
   int out_off;    // offset into the per-item partial buffer (in targets)
 };
 
+// Work lists of the shared-table rotation M2L (m2l_rot.cu, k_m2l_rot2) over one list of
+// class-grouped items: CTA groups (direction table, first item, end item) and the items' pairs
+// as (result slot, source cell, offset id, 0) records, 8 per item (slot -1: none)
+struct RotGroups {
+  DevBuf<int4> groups, vecs;
+  int n_groups = 0;
+  void build(const std::vector<int4>& items, const std::vector<int>& cpair, const std::vector<int>& pair_src,
+             const std::vector<int>& pair_off, const std::vector<int>& dir_of_off, cudaStream_t s);
+};
+
 struct Plan {
   int device = 0;
   int n_crit = 0;
@@ -82,6 +92,7 @@ struct Plan {
   // cos(theta) share one table (rot_dir maps offset -> table).
   DevBuf<double> rot, rot_geo;
   DevBuf<int> rot_dir;
+  std::vector<int> h_rot_dir;
   int n_rot_dirs = 0;
   std::vector<double> h_off;  // 3 * n_offsets
   DevBuf<double> rot_aux;  // per offset e^{-ik phi} and N!/|D|^(N+1)
@@ -108,6 +119,8 @@ struct Plan {
   // soon as the leaf basis stream ends, so these run beside the M2M levels) and the rest
   std::vector<int4> m2l_ci_leaf, m2l_ci_rest;
   DevBuf<int4> d_m2l_ci_leaf, d_m2l_ci_rest;
+  // CTA groups of the shared-table rotation M2L over each of the three item lists
+  RotGroups m2l_rg, m2l_rg_leaf, m2l_rg_rest;
   DevBuf<int> m2l_cp_leaf, m2l_cp_rest;
   std::vector<int> m2l_tgt_cells;  // target cells with >= 1 M2L source
   DevBuf<int> d_m2l_tgt_cells;

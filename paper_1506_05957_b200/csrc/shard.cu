@@ -326,6 +326,7 @@ void op_shard_setup(BemOp& op, int rank, int world, const int* tb, const int* sb
     sw.n_citems = (int)ci.size();
     sw.citems.upload(ci.empty() ? std::vector<int4>(1) : ci, s);
     sw.cpair.upload(cp.empty() ? std::vector<int>(1, 0) : cp, s);
+    if (!ci.empty()) sw.rg.build(ci, cp, pl.h_m2l_src, pl.h_m2l_off, pl.h_rot_dir, s);
   }
   // L2L: needed cells whose parent carries a local expansion (plan's pruned lists)
   std::vector<int> l2l_all;

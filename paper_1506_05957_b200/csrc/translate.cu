@@ -300,17 +300,28 @@ void tr_launch_one(int nblocks, const TrArgs& a, cudaStream_t st) {
 template <int P, int MODE>
 void tr_launch_groups(int nblocks, TrArgs a, cudaStream_t st) {
   constexpr size_t LIMIT = 227 * 1024;
-  // channel groups of 4 / 2 / 1 (Ctot = 1, 4 or 7), as large as shared memory allows
+  // channel groups of 4 / 2 / 1 (Ctot = 1, 4 or 7), as large as shared memory allows -- and as
+  // the register file allows: the 4-channel kernels of orders >= 16 and the 2-channel one of
+  // order 20 spilled 39-62 KB per thread, so those orders take narrower groups
+  constexpr int CK_MAX = P >= 20 ? 1 : P >= 16 ? 2 : 4;
   for (int cb = 0; cb < a.Ctot;) {
     const int rem = a.Ctot - cb;
     a.cbase = cb;
-    if (rem >= 4 && tr_smem<P, 4, MODE>() <= LIMIT) {
-      tr_launch_one<P, 4, MODE>(nblocks, a, st);
-      cb += 4;
-    } else if (rem >= 2 && tr_smem<P, 2, MODE>() <= LIMIT) {
-      tr_launch_one<P, 2, MODE>(nblocks, a, st);
-      cb += 2;
-    } else {
+    if constexpr (CK_MAX >= 4) {
+      if (rem >= 4 && tr_smem<P, 4, MODE>() <= LIMIT) {
+        tr_launch_one<P, 4, MODE>(nblocks, a, st);
+        cb += 4;
+        continue;
+      }
+    }
+    if constexpr (CK_MAX >= 2) {
+      if (rem >= 2 && tr_smem<P, 2, MODE>() <= LIMIT) {
+        tr_launch_one<P, 2, MODE>(nblocks, a, st);
+        cb += 2;
+        continue;
+      }
+    }
+    {
       const bool fits = tr_smem<P, 1, MODE>() <= LIMIT;
       FMM_REQUIRE(fits, "translation tiles exceed shared memory");
       tr_launch_one<P, 1, MODE>(nblocks, a, st);
@@ -585,7 +596,7 @@ void m2lg_launch(const Plan& plan, const int4* gitems, const int* gpair, int n, 
 // ------------------------------------------------------------------ launchers
 void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, double2* part,
                 cudaStream_t st, const int4* gitems, int n_gitems, const int* cells, int n_cells,
-                const int* gpair, const int4* citems, int n_citems, const int* cpair) {
+                const int* gpair, const int4* citems, int n_citems, const int* cpair, const RotGroups* rg) {
   // part holds one result block per M2L pair (CSR order): n_m2l * C * hcount(p)
   if (n_cells < 0) n_cells = plan.tgt.n_cells;
   if (plan.use_rot && p >= M2L_ROT_MIN_P && plan.rot_p >= p) {
@@ -595,8 +606,9 @@ void launch_m2l(const Plan& plan, int p, int C, const double2* M, double2* L, do
       citems = plan.d_m2l_citems.get();
       n_citems = (int)plan.m2l_citems.size();
       cpair = plan.m2l_cpair.get();
+      rg = &plan.m2l_rg;
     }
-    launch_m2l_rot(plan, citems, cpair, n_citems, p, C, M, part, st, true);
+    launch_m2l_rot(plan, citems, cpair, n_citems, p, C, M, part, st, true, rg);
   } else {
   if (!gpair) gpair = plan.m2l_gpair.get();
   if (!gitems) {

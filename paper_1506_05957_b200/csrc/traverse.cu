@@ -231,6 +231,7 @@ void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
   }
   plan.n_rot_dirs = (int)dirs.size();
   plan.rot_dir.upload(dir.empty() ? std::vector<int>(1, 0) : dir, s);
+  plan.h_rot_dir = dir;
   DevBuf<double> d_rep, geo_rep, one;
   d_rep.upload(rep.empty() ? std::vector<double>(3, 1.0) : rep, s);
   const int nd = std::max(plan.n_rot_dirs, 1);
@@ -252,8 +253,11 @@ void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
     std::vector<int> gp(plan.n_m2l);
     for (int k = 0; k < plan.n_m2l; ++k) gp[k] = k;
     std::stable_sort(gp.begin(), gp.end(), [&](int a, int b) {
-      const int ca = cls_of[plan.h_m2l_off[a]], cb = cls_of[plan.h_m2l_off[b]];
-      return ca != cb ? ca < cb : plan.h_m2l_off[a] < plan.h_m2l_off[b];
+      // by direction table first: the shared-table kernel stages one table per CTA group
+      const int oa = plan.h_m2l_off[a], ob = plan.h_m2l_off[b];
+      if (dir[oa] != dir[ob]) return dir[oa] < dir[ob];
+      const int ca = cls_of[oa], cb = cls_of[ob];
+      return ca != cb ? ca < cb : oa < ob;
     });
     for (size_t i = 0; i < gp.size();) {
       size_t j = i;
@@ -269,8 +273,9 @@ void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
     plan.h_m2l_cpair = gp;
     plan.d_m2l_citems.upload(plan.m2l_citems, s);
     plan.m2l_cpair.upload(gp, s);
+    std::vector<int> cpl_all, cpr_all;
     {
-      std::vector<int> cpl, cpr;
+      std::vector<int>&cpl = cpl_all, &cpr = cpr_all;
       plan.m2l_ci_leaf.clear();
       plan.m2l_ci_rest.clear();
       auto cut = [&](std::vector<int>& cp, std::vector<int4>& items, size_t start) {
@@ -297,6 +302,9 @@ void plan_ensure_rot(Plan& plan, int p, cudaStream_t s) {
       plan.m2l_cp_leaf.upload(cpl.empty() ? std::vector<int>(1, 0) : cpl, s);
       plan.m2l_cp_rest.upload(cpr.empty() ? std::vector<int>(1, 0) : cpr, s);
     }
+    plan.m2l_rg.build(plan.m2l_citems, gp, plan.h_m2l_src, plan.h_m2l_off, dir, s);
+    plan.m2l_rg_leaf.build(plan.m2l_ci_leaf, cpl_all, plan.h_m2l_src, plan.h_m2l_off, dir, s);
+    plan.m2l_rg_rest.build(plan.m2l_ci_rest, cpr_all, plan.h_m2l_src, plan.h_m2l_off, dir, s);
   }
 
   plan.rotf.resize((size_t)nd * rot_frag_size(p));

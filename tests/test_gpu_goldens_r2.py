@@ -140,3 +140,28 @@ def test_downward_modes_agree(name):
         out[mode] = np.load(f)
     for k in range(3):
         assert rel_l2(out["l2l"][k], out["path"][k]) <= 1e-12, k
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_shared_table_m2l_matches_reference_and_default(name):
+    """The shared-table rotation M2L (FMMBEM_M2L_SHARED=1: tables staged per CTA by bulk async
+    copies, stage C on the transposed stage-A tables) against the reference goldens and the
+    default per-warp kernel, p = 3 .. 20 (every warps-per-CTA choice), 1 and 4 channels."""
+    g = load_golden(name)
+    op, _ = _op(name)
+    x = np.random.default_rng(1).uniform(-1.0, 1.0, op.shape[0])
+    base = {p: op.apply(x, p) for p in range(3, 21)}
+    os.environ["FMMBEM_M2L_SHARED"] = "1"
+    try:
+        from paper_1506_05957_b200.configs import CONFIGS
+        from paper_1506_05957_b200.operator import GpuBemOperator
+
+        cfg = CONFIGS[name]
+        op2 = GpuBemOperator(cfg.mesh(), cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu)
+        for p in range(3, 21):
+            y = op2.apply(x, p)
+            assert rel_l2(y, base[p]) <= 1e-12, p
+            if f"apply_p{p}" in g:
+                assert rel_l2(y, g[f"apply_p{p}"]) <= 1e-10, p
+    finally:
+        os.environ.pop("FMMBEM_M2L_SHARED", None)
