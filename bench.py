@@ -466,7 +466,10 @@ def run_ours(args, cfg, mesh, world):
         "stage_share_isolated": {k: v / iso["total"] for k, v in iso.items() if k != "total"},
         "other_kernel": {
             "m2l": {"achieved": algo["m2l"] / (iso["m2l"] * 1e-3) / 1e12,
-                    "frac": algo["m2l"] / (iso["m2l"] * 1e-3) / 1e12 / fp64_peak}},
+                    "frac": algo["m2l"] / (iso["m2l"] * 1e-3) / 1e12 / fp64_peak,
+                    "note": "whole M2L stage (rotation kernel + per-target gather of the pair slots), "
+                            "averaged over the solve's orders; the rotation kernel alone at p_initial "
+                            "is in profiles/ (bound by shared-memory / L1 operand bandwidth)"}},
     }
     # apply(x, p) throughput per order (headline unit): CUDA events around
     # back-to-back device applies on the op's stream, x resident in HBM

@@ -257,11 +257,12 @@ int fmmbem_plan_evaluate(fmmbem_plan* h, const double* charges, const double* di
     Plan& pl = *h->plan;
     const int64_t ns = pl.src.n_points, nt = pl.tgt.n_points;
     cudaStream_t s = h->stream;
-    DevBuf<double> dq, dd, dpot((size_t)C * nt), dgrad(want_gradient ? (size_t)C * nt * 3 : 1);
-    if (charges) dq.upload(charges, (size_t)C * ns, s);
-    if (dipoles) dd.upload(dipoles, (size_t)C * ns * 3, s);
-    dpot.zero(s);
-    dgrad.zero(s);
+    EvalWork& w = pl.eval;  // grow-only: repeated evaluations allocate nothing
+    DevBuf<double>&dq = w.q, &dd = w.d, &dpot = w.pot, &dgrad = w.grad;
+    if (charges) dq.put(charges, (size_t)C * ns, s);
+    if (dipoles) dd.put(dipoles, (size_t)C * ns * 3, s);
+    dpot.zero_n((size_t)C * nt, s);
+    dgrad.zero_n(want_gradient ? (size_t)C * nt * 3 : 1, s);
     plan_evaluate(pl, C, charges ? dq.get() : nullptr, dipoles ? dd.get() : nullptr, p,
                   want_gradient != 0, parts, dpot.get(), want_gradient ? dgrad.get() : nullptr, s);
     FMM_CUDA(cudaMemcpyAsync(pot, dpot.get(), (size_t)C * nt * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -263,6 +263,15 @@ class DevBuf {
     if (n) FMM_CUDA(cudaMemcpyAsync(ptr_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
   }
   void upload(const std::vector<T>& v, cudaStream_t s = 0) { upload(v.data(), v.size(), s); }
+  // grow-only variants for reused workspaces: the first n elements are (re)written
+  void put(const T* h, size_t n, cudaStream_t s = 0) {
+    ensure(n);
+    if (n) FMM_CUDA(cudaMemcpyAsync(ptr_, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void zero_n(size_t n, cudaStream_t s = 0) {
+    ensure(n);
+    if (n) FMM_CUDA(cudaMemsetAsync(ptr_, 0, n * sizeof(T), s));
+  }
   std::vector<T> download(cudaStream_t s = 0) const {
     std::vector<T> h(n_);
     if (n_) {

@@ -57,7 +57,8 @@ void launch_m2l_gather(const Plan& plan, int p, int C, const double2* part, doub
 // M2M by rotation (point and shoot, DMMA): per-child contributions into cout, then the
 // children of every parent summed in order (p >= M2L_ROT_MIN_P; plan_ensure_m2m_rot first)
 void launch_m2m_rot(const Plan& plan, int p, int C, double2* M, double2* cout, cudaStream_t st);
-void launch_l2l_rot(const Plan& plan, int p, int C, double2* L, cudaStream_t st);
+// levels [l0, l1) of the target tree (default: all)
+void launch_l2l_rot(const Plan& plan, int p, int C, double2* L, cudaStream_t st, int l0 = 0, int l1 = 1 << 30);
 void launch_children_sum(const Plan& plan, int level, int CH, const double2* cout, double2* M,
                          cudaStream_t st);
 // M2M through octant-grouped child translations (cout: per-cell child contributions)
@@ -65,7 +66,7 @@ void launch_m2m_grouped(const Plan& plan, int p, int C, const double2* rfull, do
                         double2* cout, cudaStream_t st);
 // L2L into the cells listed per level whose parent has a nonzero local expansion
 void launch_l2l(const Tree& T, const std::vector<int>& level_off, const int* cells, int p, int C,
-                const double2* rfull, double2* L, cudaStream_t st);
+                const double2* rfull, double2* L, cudaStream_t st, int l0 = 1, int l1 = 1 << 30);
 
 // near field (P2P) kinds
 enum class P2PKind : int { LAP_Q = 0, LAP_D = 1, STOKESLET = 2, STRESSLET = 3 };

@@ -535,7 +535,7 @@ __host__ __device__ constexpr int rot2_warps(int P) {
 // vecs[8 item + a] = (pair slot, source cell, offset id, 0) of the item's a-th pair (slot -1:
 // none): one independent load per unit (fetched one unit ahead), then all the unit's multipoles
 // are read in one burst into the stage planes -- no dependent global loads inside the stages.
-template <int P, int W>
+template <int P, int W, bool ASYNC>
 __global__ void __launch_bounds__(W * 32)
 k_m2l_rot2(const int4* __restrict__ groups, const int4* __restrict__ vecs, const double* __restrict__ frag,
            int ttot, const double* __restrict__ aux, int aux_p, const double2* __restrict__ M, int C,
@@ -593,9 +593,32 @@ k_m2l_rot2(const int4* __restrict__ groups, const int4* __restrict__ vecs, const
                    : "memory");
     }
   };
+  // !ASYNC: the unit's multipoles in one burst of 16-byte loads (all in flight together), then
+  // stored into the planes
+  auto burst = [&](const int4& rec) {
+    const double2* mv = rec.x >= 0 ? M + ((size_t)rec.y * C + rec.w) * H : nullptr;
+    constexpr int NL = (H + 3) / 4, B = 10;
+#pragma unroll
+    for (int j0 = 0; j0 < NL; j0 += B) {
+      double2 v[B];
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int i = (lane >> 3) + 4 * (j0 + j);
+        v[j] = (mv && j0 + j < NL && i < H) ? __ldg(mv + i) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int i = (lane >> 3) + 4 * (j0 + j);
+        if (j0 + j < NL && i < H) {
+          bre[i * 8 + va] = v[j].x;
+          bim[i * 8 + va] = v[j].y;
+        }
+      }
+    }
+  };
   int unit = g.y * C + warp;
   int4 cur = fetch(unit);
-  if (cur.x != -2) {
+  if (ASYNC && cur.x != -2) {
 #pragma unroll
     for (int j = 0; j <= P; ++j) prefetch(cur, j);
   }
@@ -605,7 +628,7 @@ k_m2l_rot2(const int4* __restrict__ groups, const int4* __restrict__ vecs, const
     if (__shfl_sync(0xffffffffu, nxt.x, 0) == -1) nxt.x = -2;  // an octet past the item's vectors: skipped
     if (__shfl_sync(0xffffffffu, cur.x, 0) < 0) {  // a skipped octet: burst-load the one after it
       cur = nxt;
-      if (cur.x != -2) {
+      if (ASYNC && cur.x != -2) {
 #pragma unroll
         for (int j = 0; j <= P; ++j) prefetch(cur, j);
       }
@@ -618,6 +641,7 @@ k_m2l_rot2(const int4* __restrict__ groups, const int4* __restrict__ vecs, const
 #pragma unroll
       for (int i = lane; i <= 2 * P; i += 32) zz[i] = A[i];
     }
+    if constexpr (!ASYNC) burst(cur);
     // roles of the stages: column fr (stage A), outputs 2 fc and 2 fc + 1 (stage C)
     const int offA = __shfl_sync(0xffffffffu, cur.z, fr);
     int prO[2], offO[2], chO[2];
@@ -633,14 +657,17 @@ k_m2l_rot2(const int4* __restrict__ groups, const int4* __restrict__ vecs, const
       mbar_wait(bar, 0);  // the tables have landed
       first = false;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");  // this unit's multipoles are in the planes
+    if constexpr (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");  // this unit's multipoles are in the planes
     __syncwarp();
-    // the next unit's multipoles follow stage C through the planes, degree by degree
+    // (ASYNC) the next unit's multipoles follow stage C through the planes, degree by degree
     m2l_rot_core<P, true, true>(wsh, lane, tabs, (size_t)NT * 32, nullptr,
                                 reinterpret_cast<const double2*>(aux + (size_t)offA * astr), d0, d1,
                                 reinterpret_cast<const double2*>(aux + (size_t)offO[0] * astr),
                                 reinterpret_cast<const double2*>(aux + (size_t)offO[1] * astr),
-                                [&](int j) { prefetch(nxt, j); });
+                                [&](int j) {
+                                  if constexpr (ASYNC) prefetch(nxt, j);
+                                });
+    __syncwarp();  // the planes are free again
     cur = nxt;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -651,19 +678,22 @@ void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_
                   const double2* M, double2* pout, cudaStream_t st, bool cls, const int4* groups, int n_groups,
                   const int4* vecs) {
   constexpr int H = hcount(P);
-  // the shared-table kernel is opt-in (FMMBEM_M2L_SHARED=1): both kernels run at the same
-  // shared-memory / L1 operand bandwidth (one 256-byte fragment per DMMA), and the per-warp
-  // kernel measured 1-2 % faster end to end (cfg5 460.9 vs 456.0, cfg2 5 858 vs 5 728 mat-vecs/s)
+  // the shared-table kernel is opt-in (FMMBEM_M2L_SHARED=1; 1a = with the cp.async multipole
+  // prefetch): both kernels are bound by the LSU data pipe (operand wavefronts per DMMA: 83 % of
+  // its peak in ncu), not by L2 or latency, and the per-warp kernel measured as fast or faster
+  // (cfg5 p = 14 apply 2.461 vs 2.474 / 2.503 ms, cfg2 5 829 vs 5 739 / 5 658 mat-vecs/s)
   const char* sel = std::getenv("FMMBEM_M2L_SHARED");
   if (cls && groups && vecs && n_groups > 0 && sel && sel[0] == '1') {
     constexpr int W = rot2_warps(P);
     constexpr size_t smem2 = rot2_smem(P, W);
     static DeviceOnce attr2;
     if (attr2.first()) {
-      FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot2<P, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot2<P, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot2<P, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       attr2.mark();
     }
-    k_m2l_rot2<P, W><<<(unsigned)n_groups, W * 32, smem2, st>>>(
+    auto kern2 = sel[1] == 'a' ? k_m2l_rot2<P, W, true> : k_m2l_rot2<P, W, false>;  // "1a": cp.async prefetch
+    kern2<<<(unsigned)n_groups, W * 32, smem2, st>>>(
         groups, vecs, plan.rotf.get(), frag_base(plan.rot_p + 1), plan.rot_aux.get(), plan.rot_p, M, C, pout);
     FMM_LAUNCH_CHECK();
     return;
@@ -1141,11 +1171,11 @@ void launch_m2m_rot(const Plan& plan, int p, int C, double2* M, double2* cout, c
   }
 }
 
-void launch_l2l_rot(const Plan& plan, int p, int C, double2* L, cudaStream_t st) {
+void launch_l2l_rot(const Plan& plan, int p, int C, double2* L, cudaStream_t st, int l0, int l1) {
   FMM_REQUIRE(p >= M2L_ROT_MIN_P && p <= plan.m2m_rot_p, "rotation L2L tables not prepared");
   const VrotTabs t{plan.d_l2l_ritems.get(), plan.l2l_rchild.get(), plan.tgt.parent.get(),
                    plan.l2l_rotf.get(), plan.l2l_dir.get(), plan.l2l_aux.get(), plan.m2m_rot_p};
-  for (int l = 0; l + 1 < (int)plan.l2l_ritem_off.size(); ++l) {  // top-down
+  for (int l = std::max(l0, 0); l + 1 < (int)plan.l2l_ritem_off.size() && l < l1; ++l) {  // top-down
     const int ia = plan.l2l_ritem_off[l], ib = plan.l2l_ritem_off[l + 1];
     if (ib > ia)
       launch_vrot_dispatch<true>(std::make_integer_sequence<int, P_MAX - M2L_ROT_MIN_P + 1>{}, p, t,

@@ -477,6 +477,7 @@ bool m2m_rot_enabled() {
 // pay off only when the path epilogue's per-target work is large: cfg5 (4 088 target leaves,
 // ~80 targets each): 0.29 -> 0.11 + 0.10 ms per p = 14 apply; cfg2 / cfg3 (272 leaves): slower.
 constexpr int L2L_MIN_TGT_LEAVES = 1024;
+constexpr int L2L_ROT_MIN_CELLS = 2048;  // levels with at least this many cells take the rotation L2L
 
 bool l2l_rot_mode(const BemOp& op, int p, bool sharded, bool dense) {
   static const int force = [] {  // FMMBEM_DOWN=l2l | path
@@ -844,13 +845,26 @@ void op_layer(BemOp& op, const LayerCall& c, cudaStream_t s, bool sharded) {
 
     record(op, ST_DOWN, false, s);
     if (l2l_rot_mode(op, c.p, sharded, c.dense)) {
-      // the L2L levels hold few cells each: the dense one-CTA-per-cell kernel has the shorter
-      // critical path (FMMBEM_L2L=rot: the DMMA rotation kernel, one warp per 8 cells)
-      static const bool rot = std::getenv("FMMBEM_L2L") && std::string(std::getenv("FMMBEM_L2L")) == "rot";
-      if (rot)
-        launch_l2l_rot(pl, c.p, C, op.L.get(), s);
-      else
-        launch_l2l(pl.tgt, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s);
+      // per level: few cells -> the dense one-CTA-per-cell kernel (shorter critical path); many
+      // cells (the bottom levels of a large tree) -> the O(p^3) DMMA rotation kernel, one warp per
+      // 8 cells (cfg5 p = 14: 3 560 cells 68 us dense vs ~15 us).  FMMBEM_L2L=rot | dense forces one.
+      static const int mode = [] {
+        const char* e = std::getenv("FMMBEM_L2L");
+        return !e ? 0 : std::string(e) == "rot" ? 1 : std::string(e) == "dense" ? 2 : 0;
+      }();
+      const int nl = (int)pl.l2l_level_off.size() - 1;
+      for (int l = 1; l < nl; ++l) {
+        const int cells = pl.l2l_level_off[l + 1] - pl.l2l_level_off[l];
+        if (cells <= 0) continue;
+        static const int min_cells =
+            std::getenv("FMMBEM_L2L_ROT_MIN") ? std::atoi(std::getenv("FMMBEM_L2L_ROT_MIN")) : L2L_ROT_MIN_CELLS;
+        const bool rot = mode == 1 || (mode == 0 && cells >= min_cells);
+        if (rot)
+          launch_l2l_rot(pl, c.p, C, op.L.get(), s, l, l + 1);
+        else
+          launch_l2l(pl.tgt, pl.l2l_level_off, pl.l2l_cells.get(), c.p, C, pl.rshift_tgt.get(), op.L.get(), s, l,
+                     l + 1);
+      }
     }
     record(op, ST_DOWN, true, s);
     mark(op, 4, s);
@@ -1018,13 +1032,13 @@ void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig
   FMM_REQUIRE(C == 1 || C == 4 || C == 7, "channel count must be 1, 4 or 7");
   FMM_REQUIRE(q_orig || d_orig, "charges or dipoles required");
   const int64_t ns = plan.src.n_points;
-  DevBuf<double> qs, ds;
+  DevBuf<double>&qs = plan.eval.qs, &ds = plan.eval.ds;
   if (q_orig) {
-    qs.resize((size_t)C * ns);
+    qs.ensure((size_t)C * ns);
     k_permute_channels<<<grid_for(ns, 256), 256, 0, s>>>(ns, C, 1, plan.src.perm.get(), q_orig, qs.get());
   }
   if (d_orig) {
-    ds.resize((size_t)C * ns * 3);
+    ds.ensure((size_t)C * ns * 3);
     k_permute_channels<<<grid_for(ns, 256), 256, 0, s>>>(ns, C, 3, plan.src.perm.get(), d_orig, ds.get());
   }
   FMM_LAUNCH_CHECK();
@@ -1032,8 +1046,10 @@ void plan_evaluate(Plan& plan, int C, const double* q_orig, const double* d_orig
   if (parts & 1) {
     plan_ensure_igrid(plan, p, s);
     if (plan.use_rot) plan_ensure_rot(plan, p, s);
-    DevBuf<double2> M((size_t)plan.src.n_cells * C * hcount(p)), L((size_t)plan.tgt.n_cells * C * hcount(p));
-    DevBuf<double2> part((size_t)std::max(plan.n_m2l, 1) * C * hcount(p));
+    DevBuf<double2>&M = plan.eval.M, &L = plan.eval.L, &part = plan.eval.part;
+    M.ensure((size_t)plan.src.n_cells * C * hcount(p));
+    L.ensure((size_t)plan.tgt.n_cells * C * hcount(p));
+    part.ensure((size_t)std::max(plan.n_m2l, 1) * C * hcount(p));
     launch_p2m(S, plan.src.leaves.get(), plan.src.n_leaves, p, C, q_orig ? qs.get() : nullptr,
                d_orig ? ds.get() : nullptr, M.get(), s);
     launch_m2m(plan.src, plan.m2m_level_off, plan.m2m_cells.get(), p, C, plan.rshift_src.get(), M.get(), s);

@@ -66,8 +66,16 @@ struct RotGroups {
              const std::vector<int>& pair_off, const std::vector<int>& dir_of_off, cudaStream_t s);
 };
 
+// grow-only device workspace of plan_evaluate / fmmbem_plan_evaluate (one per plan: repeated
+// evaluations allocate nothing)
+struct EvalWork {
+  DevBuf<double> q, d, qs, ds, pot, grad;
+  DevBuf<double2> M, L, part;
+};
+
 struct Plan {
   int device = 0;
+  EvalWork eval;
   int n_crit = 0;
   int max_depth = 20;
   double theta = 0.5;

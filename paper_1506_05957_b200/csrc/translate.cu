@@ -862,7 +862,7 @@ void launch_m2m(const Tree& S, const std::vector<int>& level_off, const int* cel
 }
 
 void launch_l2l(const Tree& T, const std::vector<int>& level_off, const int* cells, int p, int C,
-                const double2* rfull, double2* L, cudaStream_t st) {
+                const double2* rfull, double2* L, cudaStream_t st, int l0, int l1) {
   TrArgs a{};
   a.parent = T.parent.get();
   a.rtab = T.rtab.get();
@@ -871,7 +871,7 @@ void launch_l2l(const Tree& T, const std::vector<int>& level_off, const int* cel
   a.in = L;
   a.out = L;
   a.Ctot = C;
-  for (int l = 1; l + 1 < (int)level_off.size(); ++l) {
+  for (int l = std::max(l0, 1); l + 1 < (int)level_off.size() && l < l1; ++l) {
     a.cells = cells + level_off[l];
     tr_dispatch<T_L2L>(p, level_off[l + 1] - level_off[l], a, st);
   }

@@ -142,16 +142,17 @@ def test_downward_modes_agree(name):
         assert rel_l2(out["l2l"][k], out["path"][k]) <= 1e-12, k
 
 
-@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
-def test_shared_table_m2l_matches_reference_and_default(name):
+@pytest.mark.parametrize("name,variant", [("cfg2", "1"), ("cfg3", "1"), ("cfg2", "1a")])
+def test_shared_table_m2l_matches_reference_and_default(name, variant):
     """The shared-table rotation M2L (FMMBEM_M2L_SHARED=1: tables staged per CTA by bulk async
-    copies, stage C on the transposed stage-A tables) against the reference goldens and the
-    default per-warp kernel, p = 3 .. 20 (every warps-per-CTA choice), 1 and 4 channels."""
+    copies, stage C on the transposed stage-A tables; 1a: the multipoles prefetched by cp.async)
+    against the reference goldens and the default per-warp kernel, p = 3 .. 20 (every
+    warps-per-CTA choice), 1 and 4 channels."""
     g = load_golden(name)
     op, _ = _op(name)
     x = np.random.default_rng(1).uniform(-1.0, 1.0, op.shape[0])
     base = {p: op.apply(x, p) for p in range(3, 21)}
-    os.environ["FMMBEM_M2L_SHARED"] = "1"
+    os.environ["FMMBEM_M2L_SHARED"] = variant
     try:
         from paper_1506_05957_b200.configs import CONFIGS
         from paper_1506_05957_b200.operator import GpuBemOperator
