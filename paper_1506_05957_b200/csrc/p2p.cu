@@ -208,8 +208,14 @@ k_p2p(TreeDev S, TreeDev T, const P2PItem* __restrict__ items, const int* __rest
 // warp's reduction of item k overlaps the other warps' item k + 1); EMPTY is a named barrier
 // (consumers arrive, producers sync).
 constexpr int LAPD_TPT = 4;
-constexpr int LAPD_CONS = 256;
-constexpr int LAPD_PROD = 128;
+#ifndef LAPD_CONS_N
+#define LAPD_CONS_N 256
+#endif
+constexpr int LAPD_CONS = LAPD_CONS_N;  // consumer threads (tools: -DLAPD_CONS_N=384)
+#ifndef LAPD_PROD_N
+#define LAPD_PROD_N 128
+#endif
+constexpr int LAPD_PROD = LAPD_PROD_N;
 #ifndef LAPD_SPT
 #define LAPD_SPT 2  // sources per trip of the consumer loop (tools: -DLAPD_SPT=3)
 #endif
