@@ -771,8 +771,11 @@ __global__ void k_m2m_aux(const double* __restrict__ geo, int n_off, int P, doub
 //   input phase e^{+ik phi}), translate along z with the upper-triangular Toeplitz
 //   L''_n^k = sum_{j>=n} |d|^{j-n}/(j-n)! L'_j^k, and rotate back with A^T = E a^T (the M2L's
 //   stage C).
+#ifndef VROT_MIN_BLOCKS
+#define VROT_MIN_BLOCKS 1
+#endif
 template <int P, bool LOCAL>
-__global__ void __launch_bounds__(ROT_WARPS * 32)
+__global__ void __launch_bounds__(ROT_WARPS * 32, VROT_MIN_BLOCKS)
 k_vrot(const int4* __restrict__ items, int n_items, const int* __restrict__ child,
        const int* __restrict__ parent, const double* __restrict__ frag, const int* __restrict__ dir,
        int ttot, const double* __restrict__ aux, int aux_p, const double2* __restrict__ in, int C,

@@ -368,8 +368,16 @@ __device__ __forceinline__ void lapd_run_clusters(const double2* __restrict__ sh
   lapd_body_cl<TPT, C>(u, tx, ty, tz, tt, acc);
 }
 
+// The launch bound is 128 threads above the launched count, which caps the kernel at 128
+// registers per thread (no spills; 149 uncapped).  Alone the kernel is 1.6 % slower (1.482 vs
+// 1.458 ms on cfg5), but the 16 K registers it leaves per SM let the far-field CTAs (basis
+// stream, rotation M2M, M2L) co-reside: the upward pass ends under the near field instead of
+// 0.19 ms after it (cfg5 465 -> 473 mat-vecs/s, cfg2 5 850 -> 6 050; 96 registers spill: 408).
+#ifndef LAPD_BOUND_EXTRA
+#define LAPD_BOUND_EXTRA 128
+#endif
 template <int NCT, int NSTG>
-__global__ void __launch_bounds__(NCT + LAPD_PROD, 1)
+__global__ void __launch_bounds__(NCT + LAPD_PROD + LAPD_BOUND_EXTRA, 1)
 k_p2p_lapd(TreeDev T, const LapdHdr* __restrict__ hdrs, int n_items, const int4* __restrict__ gl_ltab,
            const int* __restrict__ gl_slot, const int* __restrict__ gl_spec, int max_src, int max_leaves, int max_tgt,
            const double2* __restrict__ srec, const int* __restrict__ s_panel, const int* __restrict__ s_code,
