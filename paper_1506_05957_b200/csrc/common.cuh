@@ -231,6 +231,42 @@ __device__ inline void irregular_half(double x, double y, double z, int p, doubl
   }
 }
 
+// ---------------------------------------------------------------- bulk async copies (TMA)
+// mbarrier + cp.async.bulk helpers (sm_90+): one thread arms the barrier with the byte count and
+// issues the copies; every consumer polls the barrier's phase.
+__device__ __forceinline__ void tma_bar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_bar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "TMAW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TMAW_%=;\n"
+      "}\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared, 16-byte aligned, a multiple of 16 bytes; completes on the mbarrier
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+// generic-proxy reads of a shared buffer are ordered before the async-proxy writes that refill it
+__device__ __forceinline__ void tma_fence_proxy() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // ---------------------------------------------------------------- device buffer
 template <typename T>
 class DevBuf {

@@ -771,11 +771,16 @@ __global__ void k_m2m_aux(const double* __restrict__ geo, int n_off, int P, doub
 //   input phase e^{+ik phi}), translate along z with the upper-triangular Toeplitz
 //   L''_n^k = sum_{j>=n} |d|^{j-n}/(j-n)! L'_j^k, and rotate back with A^T = E a^T (the M2L's
 //   stage C).
-#ifndef VROT_MIN_BLOCKS
-#define VROT_MIN_BLOCKS 1
+// The M2M instance is bounded to 128 registers per thread (8 CTAs of 64 threads per SM; 24-32
+// bytes of spills at the high orders, 254 registers uncapped): its levels run beside the
+// persistent near field, which leaves 16 K registers per SM -- two M2M CTAs instead of one, and
+// the chain ends under the near field instead of after it.  The L2L instance runs after the
+// near field and keeps the whole register file.
+#ifndef VROT_M2M_MIN_BLOCKS
+#define VROT_M2M_MIN_BLOCKS 8
 #endif
 template <int P, bool LOCAL>
-__global__ void __launch_bounds__(ROT_WARPS * 32, VROT_MIN_BLOCKS)
+__global__ void __launch_bounds__(ROT_WARPS * 32, LOCAL ? 1 : VROT_M2M_MIN_BLOCKS)
 k_vrot(const int4* __restrict__ items, int n_items, const int* __restrict__ child,
        const int* __restrict__ parent, const double* __restrict__ frag, const int* __restrict__ dir,
        int ttot, const double* __restrict__ aux, int aux_p, const double2* __restrict__ in, int C,

@@ -15,6 +15,7 @@
 // shuffle-tree reduction in a fixed order.
 #include <algorithm>
 
+#include <string>
 #include "operator.cuh"
 
 namespace fmmbem {
@@ -191,6 +192,102 @@ k_p2m_basis_cl(const int4* __restrict__ items, const int* __restrict__ red_of,
     M[(size_t)rc.x * H + h] = acc;
   }
   if (threadIdx.x == 0) arrive[r] = 0u;
+}
+
+// The same stream through the TMA: one thread arms an mbarrier and issues bulk async copies of
+// P2M_TMA_ROWS rows at a time into a two-deep shared-memory ring; the CTA's threads (one per
+// coefficient column) accumulate the rows in entry order.  The copy engine generates the
+// addresses, so the stream needs almost no issue slots -- it runs beside the persistent near
+// field, whose warps otherwise starve a load-issuing kernel (basis stream 0.98 ms beside the
+// near field with k_p2m_basis_cl).
+constexpr int P2M_TMA_ROWS = 8;
+
+template <int NJ>
+__global__ void __launch_bounds__(128)
+k_p2m_basis_tma(const int4* __restrict__ items, const int* __restrict__ red_of,
+                const int4* __restrict__ reds, unsigned* arrive, int Hp, int H,
+                const double2* __restrict__ B, const int* __restrict__ e_panel,
+                const double* __restrict__ x, double2* __restrict__ M, double2* __restrict__ part) {
+  constexpr int R = P2M_TMA_ROWS;
+  extern __shared__ __align__(128) unsigned char p2m_smem[];
+  double2* buf = reinterpret_cast<double2*>(p2m_smem);  // [2][R][H]
+  __shared__ double sx[P2M_CHUNK];
+  __shared__ unsigned long long full[2];
+  const int4 it = items[blockIdx.x];
+  const int len = it.z - it.y, tid = threadIdx.x;
+  if (tid < len) sx[tid] = __ldg(x + __ldg(e_panel + it.y + tid));
+  if (tid == 0) {
+    tma_bar_init(&full[0], 1);
+    tma_bar_init(&full[1], 1);
+    tma_bar_init_fence();
+  }
+  __syncthreads();
+  const int nchunk = (len + R - 1) / R;
+  auto issue = [&](int c) {  // (thread 0) chunk c into ring slot c & 1
+    const int r0 = c * R, nr = min(R, len - r0);
+    unsigned long long* bar = &full[c & 1];
+    double2* dst = buf + (size_t)(c & 1) * R * H;
+    const double2* src = B + (size_t)(it.y + r0) * Hp;
+    tma_bar_expect(bar, (unsigned)(nr * H * sizeof(double2)));
+    if (H == Hp) {
+      tma_load_1d(dst, src, (unsigned)(nr * H * sizeof(double2)), bar);
+    } else {
+      for (int r = 0; r < nr; ++r)
+        tma_load_1d(dst + (size_t)r * H, src + (size_t)r * Hp, (unsigned)(H * sizeof(double2)), bar);
+    }
+  };
+  if (tid == 0) {
+    issue(0);
+    if (nchunk > 1) issue(1);
+  }
+  double2 acc[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) acc[j] = make_double2(0.0, 0.0);
+  for (int c = 0; c < nchunk; ++c) {
+    tma_bar_wait(&full[c & 1], (unsigned)(c >> 1) & 1u);
+    const double2* b = buf + (size_t)(c & 1) * R * H;
+    const int nr = min(R, len - c * R);
+    for (int r = 0; r < nr; ++r) {
+      const double s = sx[c * R + r];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int h = tid + 128 * j;
+        if (h < H) {
+          const double2 v = b[(size_t)r * H + h];
+          acc[j].x = fma(s, v.x, acc[j].x);
+          acc[j].y = fma(s, v.y, acc[j].y);
+        }
+      }
+    }
+    __syncthreads();  // the ring slot is consumed
+    if (tid == 0 && c + 2 < nchunk) {
+      tma_fence_proxy();
+      issue(c + 2);
+    }
+  }
+  double2* out = it.w < 0 ? M + (size_t)it.x * H : part + (size_t)it.w * H;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int h = tid + 128 * j;
+    if (h < H) out[h] = acc[j];
+  }
+  if (it.w < 0) return;
+  // a cell split over several items: the last one to finish adds the partials in slot order
+  const int r = red_of[blockIdx.x];
+  const int4 rc = reds[r];
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(arrive + r, 1u) == (unsigned)rc.z - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int h = tid; h < H; h += blockDim.x) {
+    double2 a = __ldcg(part + (size_t)rc.y * H + h);
+    for (int k = 1; k < rc.z; ++k) a = cadd(a, __ldcg(part + (size_t)(rc.y + k) * H + h));
+    M[(size_t)rc.x * H + h] = a;
+  }
+  if (tid == 0) arrive[r] = 0u;
 }
 
 // Direct upward basis: entry e = (cell, cluster in the cell's subtree),
@@ -391,7 +488,31 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
     const P2MItems& red = direct ? op.p2m_reduce : op.p2m_leaf_reduce;
     FMM_REQUIRE(op.p2m_part.size() >= (size_t)std::max(op.n_p2m_slots, op.n_p2m_leaf_slots) * H,
                 "P2M partial buffer not sized");
-    if (it.n) {
+    // the TMA stream from 1 024 items up (small problems are latency-bound: the load-issuing
+    // kernel starts faster, cfg1 18.5 k vs 17.9 k mat-vecs/s); FMMBEM_P2M=ldg | tma forces one
+    static const int force = [] {
+      const char* e = std::getenv("FMMBEM_P2M");
+      return !e ? 0 : std::string(e) == "ldg" ? 1 : std::string(e) == "tma" ? 2 : 0;
+    }();
+    const bool use_tma = force == 2 || (force == 0 && it.n >= 1024);
+    if (it.n && use_tma) {
+      const int Hp = hcount(op.basis_p);
+      const size_t smem = (size_t)2 * P2M_TMA_ROWS * H * sizeof(double2);
+      static DeviceOnce attr;
+      if (attr.first()) {
+        FMM_CUDA(cudaFuncSetAttribute(k_p2m_basis_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        FMM_CUDA(cudaFuncSetAttribute(k_p2m_basis_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        attr.mark();
+      }
+      if (H <= 128)
+        k_p2m_basis_tma<1><<<it.n, 128, smem, s>>>(it.d.get(), it.red_of.get(), red.d.get(), it.arrive.get(), Hp,
+                                                   H, op.p2m_basis.get(), op.cl_panel.get(), x, M,
+                                                   op.p2m_part.get());
+      else
+        k_p2m_basis_tma<2><<<it.n, 128, smem, s>>>(it.d.get(), it.red_of.get(), red.d.get(), it.arrive.get(), Hp,
+                                                   H, op.p2m_basis.get(), op.cl_panel.get(), x, M,
+                                                   op.p2m_part.get());
+    } else if (it.n) {
       const int nj = (H + 31) / 32, Hp = hcount(op.basis_p);
 #define P2M_CL(NJ)                                                                              \
   case NJ:                                                                                      \

@@ -801,7 +801,9 @@ void launch_p2p_lapd(const TreeDev& T, const P2PAux& aux, int max_src, const dou
   // shared-memory carveout of the SMs this persistent kernel occupies: the far-field kernels
   // launched beside it can only co-reside in what the configuration leaves over
   // (FMMBEM_P2P_CARVEOUT=percent, -1 = driver default)
-  static const int carve = std::getenv("FMMBEM_P2P_CARVEOUT") ? std::atoi(std::getenv("FMMBEM_P2P_CARVEOUT")) : -1;
+  // default: the maximum -- with the driver's choice (164 KB for this kernel's 150 KB) a far-field
+  // CTA that needs more than ~12 KB of shared memory cannot be placed beside it
+  static const int carve = std::getenv("FMMBEM_P2P_CARVEOUT") ? std::atoi(std::getenv("FMMBEM_P2P_CARVEOUT")) : 100;
   if (carve >= 0)
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
   int dev = 0, sms = 0;
