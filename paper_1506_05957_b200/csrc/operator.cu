@@ -617,6 +617,9 @@ void op_init(BemOp& op, const double* panel_vertices, int64_t P, const double* g
   op.fine_w.upload(fine_wts, 19 * P, s);
   op.leg_x.upload(leg_x, n_gauss_singular, s);
   op.leg_w.upload(leg_w, n_gauss_singular, s);
+  // large double-layer systems: 1 024-source items for the persistent near-field kernel (fewer
+  // item hand-overs; 896 is the better tile below ~100 k panels and for the other kernels)
+  if (formulation == LAPLACE_SECOND && 4 * P >= 400000 && !std::getenv("FMMBEM_P2P_ITEM")) op.plan.p2p_item_src = 1024;
   plan_build(op.plan, gauss_pts, 4 * P, cen.data(), P, n_crit, theta, max_depth, s);
   const int64_t ns = op.plan.src.n_points;
   op.s_weight.resize(ns);

@@ -76,6 +76,10 @@ struct EvalWork {
 struct Plan {
   int device = 0;
   EvalWork eval;
+  // sources per P2P work item: 0 = p2p_item_sources(); the operator sets 1 024 for large
+  // double-layer systems (the persistent near-field kernel: cfg5 493.6 -> 500.3 mat-vecs/s)
+  int p2p_item_src = 0;
+  int item_sources() const { return p2p_item_src > 0 ? p2p_item_src : p2p_item_sources(); }
   int n_crit = 0;
   int max_depth = 20;
   double theta = 0.5;

@@ -263,9 +263,9 @@ void op_shard_setup(BemOp& op, int rank, int world, const int* tb, const int* sb
     ib[li] = (int)sw.items_h.size();
     int b = pl.h_p2p_row[t];
     const int e = pl.h_p2p_row[t + 1];
-    while (b < e) {  // same slicing rule as plan_make_items (<= p2p_item_sources() sources)
+    while (b < e) {  // same slicing rule as plan_make_items (<= Plan::item_sources() sources)
       int acc = 0, k = b;
-      while (k < e && (acc == 0 || acc + S.h_body_count[pl.h_p2p_src[k]] <= p2p_item_sources())) {
+      while (k < e && (acc == 0 || acc + S.h_body_count[pl.h_p2p_src[k]] <= pl.item_sources())) {
         acc += S.h_body_count[pl.h_p2p_src[k]];
         ++k;
       }

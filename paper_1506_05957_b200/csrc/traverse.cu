@@ -428,7 +428,7 @@ void plan_build(Plan& plan, const double* src_xyz, int64_t ns, const double* tgt
   plan.p2p_row.upload(plan.h_p2p_row, s);
   plan.p2p_src.upload(plan.h_p2p_src, s);
   std::vector<int> item_begin;
-  plan_make_items(T, S, plan.h_p2p_row, plan.h_p2p_src, p2p_item_sources(), plan.items, item_begin,
+  plan_make_items(T, S, plan.h_p2p_row, plan.h_p2p_src, plan.item_sources(), plan.items, item_begin,
                   plan.part_len, plan.p2p_interactions);
   plan.d_items.upload(plan.items, s);
   {
