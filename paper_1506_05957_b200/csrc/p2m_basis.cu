@@ -200,7 +200,10 @@ k_p2m_basis_cl(const int4* __restrict__ items, const int* __restrict__ red_of,
 // addresses, so the stream needs almost no issue slots -- it runs beside the persistent near
 // field, whose warps otherwise starve a load-issuing kernel (basis stream 0.98 ms beside the
 // near field with k_p2m_basis_cl).
-constexpr int P2M_TMA_ROWS = 8;
+#ifndef P2M_TMA_ROWS_N
+#define P2M_TMA_ROWS_N 8
+#endif
+constexpr int P2M_TMA_ROWS = P2M_TMA_ROWS_N;
 
 template <int NJ>
 __global__ void __launch_bounds__(128)
