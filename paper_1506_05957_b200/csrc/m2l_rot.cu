@@ -155,7 +155,10 @@ __device__ __forceinline__ void dmma(double2& d, double a, double b) {
                : "d"(a), "d"(b));
 }
 
-constexpr int ROT_WARPS = 2;
+#ifndef ROT_WARPS_N
+#define ROT_WARPS_N 2
+#endif
+constexpr int ROT_WARPS = ROT_WARPS_N;  // warp units per CTA of the per-warp rotation kernels
 constexpr int FRAG_KS_MAX = (P_MAX + 4) / 4;  // k-steps of the largest degree
 static_assert((P_MAX + 8) / 8 <= 3, "row tiles per degree");
 

@@ -35,6 +35,15 @@ def main():
         st = sum(float(r[i_s] or 0) for r in rs)
         print(f"exec {e:>10d} x {len(rs):4d} instr  stall samples {st / tot * 100:5.1f}%  "
               + ", ".join(f"{k} {v}" for k, v in sorted(mix.items(), key=lambda x: -x[1])))
+        # stall reasons of the group (share of the group's samples)
+        reasons = {}
+        for i, nme in enumerate(h):
+            if nme.startswith("stall_") and "Not Issued" not in nme:
+                v = sum(float(r[i] or 0) for r in rs if i < len(r))
+                if v:
+                    reasons[nme[6:]] = v
+        tr = sum(reasons.values()) or 1.0
+        print("      " + ", ".join(f"{k} {v / tr * 100:.0f}%" for k, v in sorted(reasons.items(), key=lambda x: -x[1])[:7]))
 
 
 if __name__ == "__main__":
