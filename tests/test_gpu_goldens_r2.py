@@ -166,3 +166,32 @@ def test_shared_table_m2l_matches_reference_and_default(name, variant):
                 assert rel_l2(y, g[f"apply_p{p}"]) <= 1e-10, p
     finally:
         os.environ.pop("FMMBEM_M2L_SHARED", None)
+
+
+def test_basis_stream_kernels_agree():
+    """The upward basis stream by bulk async copies (TMA ring, the default from 1 024 items) and by
+    per-thread loads (FMMBEM_P2M=ldg) give the same mat-vec; the switch is read once per process,
+    so each runs in a subprocess (cfg2: direct-basis mode, 85 k entries)."""
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, sys; sys.path.insert(0, '.');"
+            "from paper_1506_05957_b200.configs import CONFIGS;"
+            "from paper_1506_05957_b200.operator import GpuBemOperator;"
+            "cfg = CONFIGS['cfg2'];"
+            "op = GpuBemOperator(cfg.mesh(), cfg.formulation, theta=cfg.theta, n_crit=cfg.n_crit, mu=cfg.mu);"
+            "x = np.random.default_rng(1).uniform(-1, 1, op.shape[0]);"
+            "np.save(sys.argv[1], np.stack([op.apply(x, p) for p in (3, 5, 12, 16)]))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("tma", "ldg"):
+        f = os.path.join(root, "gpurun_out", f"basis_{mode}.npy")
+        os.makedirs(os.path.dirname(f), exist_ok=True)
+        subprocess.run([sys.executable, "-c", code, f], cwd=root, check=True,
+                       env=dict(os.environ, FMMBEM_P2M=mode))
+        out[mode] = np.load(f)
+    g = load_golden("cfg2")
+    for i, p in enumerate((3, 5, 12, 16)):
+        assert rel_l2(out["tma"][i], out["ldg"][i]) <= 1e-12, p
+        if f"apply_p{p}" in g:
+            assert rel_l2(out["tma"][i], g[f"apply_p{p}"]) <= 1e-10, p
