@@ -706,6 +706,12 @@ void launch_rot_p(const Plan& plan, const int4* gitems, const int* gpair, int n_
   if (attr.first()) {
     FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    // FMMBEM_M2L_CARVEOUT=percent: shared-memory share of the SM for this kernel (fewer resident
+    // CTAs, more L1 for the table fragments); default: the driver's choice
+    if (const char* e = std::getenv("FMMBEM_M2L_CARVEOUT")) {
+      FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P, false>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
+      FMM_CUDA(cudaFuncSetAttribute(k_m2l_rot<P, true>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e)));
+    }
     attr.mark();
   }
   const int64_t units = (int64_t)n_items * C;
