@@ -115,6 +115,82 @@ k_p2m_basis(const int* __restrict__ leaves, const int* __restrict__ body_start,
   }
 }
 
+// The same sums with the leaf's channel scalars staged once in shared memory (the kernel above
+// recomputes them for every coefficient: ~25 instructions per 16-byte table entry) and two
+// coefficient rows per warp in flight, up to 4 entries per lane each.  Per-lane order and the
+// lane reduction are those of k_p2m_basis, so the results are bit-identical.
+template <int C>
+__global__ void __launch_bounds__(256)
+k_p2m_basis_st(const int* __restrict__ leaves, const int* __restrict__ body_start,
+               const int* __restrict__ body_count, int64_t ns, int H, int kind,
+               const double2* __restrict__ B, const int* __restrict__ s_panel,
+               const double* __restrict__ x, const double* __restrict__ px,
+               const double* __restrict__ py, const double* __restrict__ pz,
+               double2* __restrict__ M, int max_nb) {
+  extern __shared__ double p2m_ss[];  // [C][max_nb]
+  const int leaf = leaves[blockIdx.x];
+  const int b0 = body_start[leaf], nb = body_count[leaf];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    double s[C == 1 ? 1 : 4];
+    basis_scalars<C>(kind, b0 + b, s_panel, x, px, py, pz, s);
+#pragma unroll
+    for (int c = 0; c < C; ++c) p2m_ss[c * max_nb + b] = s[c];
+  }
+  __syncthreads();
+  constexpr int U = 4;  // entries per lane in flight per row
+  for (int idx = warp; idx < H; idx += 2 * nw) {
+    const int idx2 = idx + nw;
+    const bool two = idx2 < H;
+    double2 acc[2][C];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[r][c] = make_double2(0.0, 0.0);
+    const double2* B0 = B + (size_t)idx * ns + b0;
+    const double2* B1 = B + (size_t)(two ? idx2 : idx) * ns + b0;
+    for (int bb = lane; bb < nb; bb += 32 * U) {
+      double2 v0[U], v1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = bb + 32 * u;
+        v0[u] = b < nb ? __ldg(B0 + b) : make_double2(0.0, 0.0);
+        v1[u] = (two && b < nb) ? __ldg(B1 + b) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = bb + 32 * u;
+        if (b < nb) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            const double sc = p2m_ss[c * max_nb + b];
+            acc[0][c].x = fma(sc, v0[u].x, acc[0][c].x);
+            acc[0][c].y = fma(sc, v0[u].y, acc[0][c].y);
+            acc[1][c].x = fma(sc, v1[u].x, acc[1][c].x);
+            acc[1][c].y = fma(sc, v1[u].y, acc[1][c].y);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        for (int o = 16; o > 0; o >>= 1) {
+          acc[r][c].x += __shfl_xor_sync(0xffffffffu, acc[r][c].x, o);
+          acc[r][c].y += __shfl_xor_sync(0xffffffffu, acc[r][c].y, o);
+        }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        M[((size_t)leaf * C + c) * H + idx] = acc[0][c];
+        if (two) M[((size_t)leaf * C + c) * H + idx2] = acc[1][c];
+      }
+    }
+  }
+}
+
 // clustered entries (Laplace kinds, one channel), entry-major Bd[e][h]: work item
 // (cell, entry range, slot): acc[h] = sum_e Bd[e][h] x[panel(e)], one thread per h;
 // slot < 0 writes the cell's multipole, else a partial that k_p2m_reduce adds in order
@@ -535,6 +611,23 @@ void launch_p2m_basis(BemOp& op, int p, int C, const double* x, double2* M, cuda
       n_leaves = S.n_leaves;
     }
     if (n_leaves <= 0) return;
+    const int max_nb = std::max(S.max_leaf_count, 1);
+    const size_t ss_bytes = (size_t)C * max_nb * sizeof(double);
+    static const bool old_kernel = std::getenv("FMMBEM_P2M_BASIS") && std::string(std::getenv("FMMBEM_P2M_BASIS")) == "old";
+    if (ss_bytes <= 48 * 1024 && !old_kernel) {
+      if (C == 1)
+        k_p2m_basis_st<1><<<n_leaves, 256, ss_bytes, s>>>(leaves, S.body_start.get(), S.body_count.get(), S.n_points,
+                                                           H, op.basis_kind_for_sys, op.p2m_basis.get(),
+                                                           op.s_panel.get(), x, S.px.get(), S.py.get(), S.pz.get(), M,
+                                                           max_nb);
+      else
+        k_p2m_basis_st<4><<<n_leaves, 256, ss_bytes, s>>>(leaves, S.body_start.get(), S.body_count.get(), S.n_points,
+                                                           H, op.basis_kind_for_sys, op.p2m_basis.get(),
+                                                           op.s_panel.get(), x, S.px.get(), S.py.get(), S.pz.get(), M,
+                                                           max_nb);
+      FMM_LAUNCH_CHECK();
+      return;
+    }
     if (C == 1)
     k_p2m_basis<1><<<n_leaves, 256, 0, s>>>(leaves, S.body_start.get(), S.body_count.get(),
                                               S.n_points, H, op.basis_kind_for_sys,
